@@ -1,0 +1,172 @@
+/*
+ * tsdf_b200.h -- C ABI of the B200 (sm_100a) TSDF-fusion hot path.
+ *
+ * Drop-in boundary for the reference package's hot path
+ * (/root/reference/pkg/src/tsdfusion).  Plain pointers and sizes only; no
+ * torch or CUDA C++ types.  Every entry point returns an int status whose
+ * values are the reference's FusionError exit codes (errors.py:4-37):
+ *   0 ok, 2 ConfigError, 3 DatasetError, 4 CapacityError, 5 NotFoundError,
+ *   6 FormatError, 8 ValueError (Python builtin), 9 CUDA/driver failure.
+ * tsdf_last_error() returns a message for the calling thread's last failure.
+ *
+ * Threading: one host thread per table; every call enqueues on the table's
+ * CUDA stream and returns after its results are on the host.
+ * Ownership: the table owns all device memory; callers own input buffers
+ * for the duration of a call.  `mem` says where input buffers live
+ * (TSDF_MEM_HOST: pageable/pinned host memory, copied inside the call;
+ * TSDF_MEM_DEVICE: device pointers, read in place).
+ */
+#ifndef TSDF_B200_H
+#define TSDF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSDF_OK 0
+#define TSDF_ECONFIG 2
+#define TSDF_EDATASET 3
+#define TSDF_ECAPACITY 4
+#define TSDF_ENOTFOUND 5
+#define TSDF_EFORMAT 6
+#define TSDF_EVALUE 8
+#define TSDF_ECUDA 9
+
+/* element types of input buffers */
+#define TSDF_F64 0
+#define TSDF_F32 1
+#define TSDF_U8 2  /* colour channels: value/255.0, as datasets.py:118,163 */
+#define TSDF_U16 3
+
+#define TSDF_MEM_HOST 0
+#define TSDF_MEM_DEVICE 1
+
+typedef struct tsdf_table tsdf_table;
+
+/* IntegrationStats (reference integrate.py:42-50) */
+typedef struct {
+  int64_t measurements;
+  int64_t skipped_invalid;
+  int64_t blocks_allocated;
+  int64_t blocks_touched;
+  int64_t voxels_updated;
+  int64_t observations;
+  int32_t no_valid_warning; /* "frame has no valid depth pixels" */
+  int32_t pad;
+} tsdf_integration_stats;
+
+/* MergeStats (reference adapt.py:20-23) */
+typedef struct {
+  int64_t candidates;
+  int64_t merged;
+} tsdf_merge_stats;
+
+/* Mesh (reference meshing.py:39-59); arrays owned by the library until
+ * tsdf_mesh_free(). */
+typedef struct {
+  double *vertices;   /* nv x 3, metres */
+  double *normals;    /* nv x 3, unit */
+  double *colors;     /* nv x 3, [0, 1] */
+  int64_t num_vertices;
+  int64_t *triangles; /* nt x 3 */
+  int64_t num_triangles;
+} tsdf_mesh;
+
+/* HashTable(n_hash, bucket_capacity, overflow_capacity, block_edge,
+ * heap_capacities) -- reference hashgrid.py:142-165.  `cuda_stream` may be
+ * NULL (the table creates its own non-blocking stream). */
+int tsdf_table_create(int64_t n_hash, int32_t bucket_capacity, int32_t overflow_capacity,
+                      double block_edge, int32_t n_levels, const int64_t *heap_capacities,
+                      void *cuda_stream, tsdf_table **out);
+int tsdf_table_destroy(tsdf_table *t);
+/* drop every block (fresh table, same sizes) */
+int tsdf_table_reset(tsdf_table *t);
+/* block-key-hash sharding: this table owns only keys with
+ * owner(key) == rank (world > 1); DESIGN.md "Multi-GPU". */
+int tsdf_table_set_shard(tsdf_table *t, int32_t rank, int32_t world);
+
+/* integrate_depth(table, DepthFrame, tau, weight_cap) -- integrate.py:255-342.
+ * depth: H*W z-depth in metres (0 / NaN invalid); rgb: H*W*3 or NULL.
+ * K = (fx, fy, cx, cy); R row-major 3x3 and t (3) are world-from-sensor
+ * (geometry.py:12-34). */
+int tsdf_integrate_depth(tsdf_table *t, const void *depth, int32_t depth_dtype, const void *rgb,
+                         int32_t rgb_dtype, int32_t height, int32_t width, int32_t mem,
+                         const double *K, const double *R, const double *trans, double tau,
+                         double weight_cap, tsdf_integration_stats *stats);
+
+/* integrate_pointcloud(table, PointCloudFrame, tau, weight_cap) --
+ * integrate.py:175-252.  xyz: n*3 sensor-frame points; rgb n*3 or NULL. */
+int tsdf_integrate_points(tsdf_table *t, const void *xyz, int32_t xyz_dtype, const void *rgb,
+                          int32_t rgb_dtype, int64_t n, int32_t mem, const double *R,
+                          const double *trans, double tau, double weight_cap,
+                          tsdf_integration_stats *stats);
+
+/* allocate_for_measurement(table, origin, p, tau) -- integrate.py:143-161.
+ * Writes up to max_out handles in traversal order; *n_out = total count. */
+int tsdf_allocate_for_measurement(tsdf_table *t, const double *origin, const double *p,
+                                  double tau, int64_t *handles, int64_t max_out, int64_t *n_out);
+
+/* apply_merges(table, sigma_threshold, min_eligible_fraction,
+ * min_mean_weight) -- adapt.py:119-136.  all_levels = 0 reproduces the
+ * reference (level 0 -> 1 only); 1 enables the labelled multi-level
+ * extension (every level L -> L+1, candidates snapshotted per pass). */
+int tsdf_apply_merges(tsdf_table *t, double sigma_threshold, double min_eligible_fraction,
+                      double min_mean_weight, int32_t all_levels, tsdf_merge_stats *stats);
+
+/* extract_mesh(table, iso, collapse_epsilon) -- meshing.py:412-487.
+ * collapse_epsilon < 0 selects the default 0.25 * voxel_size(0). */
+int tsdf_extract_mesh(tsdf_table *t, double iso, double collapse_epsilon, tsdf_mesh *out);
+void tsdf_mesh_free(tsdf_mesh *m);
+
+/* HashTable.find_batch (hashgrid.py:300-331) */
+int tsdf_find_batch(tsdf_table *t, const int64_t *coords, int64_t n, int64_t *handles,
+                    int32_t *levels, uint8_t *found);
+/* HashTable.insert (hashgrid.py:212-251): idempotent, zero-initialised */
+int tsdf_insert(tsdf_table *t, const int64_t *coord, int32_t level, int64_t *handle);
+/* HashTable.remove (hashgrid.py:253-283): returns the payload (any pointer
+ * may be NULL); buffers hold nvox(level) voxels, colour interleaved rgb */
+int tsdf_remove(tsdf_table *t, const int64_t *coord, int32_t *level, double *tsdf,
+                double *weight, double *s2, float *color);
+/* BlockHeap.payload / write_payload (hashgrid.py:115-133) by coordinate */
+int tsdf_read_block(tsdf_table *t, const int64_t *coord, int32_t *level, double *tsdf,
+                    double *weight, double *s2, float *color);
+int tsdf_write_block(tsdf_table *t, const int64_t *coord, const double *tsdf,
+                     const double *weight, const double *s2, const float *color);
+/* BlockHeap.occupied for one level */
+int tsdf_live_count(tsdf_table *t, int32_t level, int64_t *n);
+/* all live blocks of a level in canonical (x, y, z) order with their
+ * payloads (parity export / save_map).  Call with coords == NULL to get the
+ * count in *n_out. */
+int tsdf_export_level(tsdf_table *t, int32_t level, int64_t max_blocks, int64_t *coords,
+                      int64_t *handles, double *tsdf, double *weight, double *s2, float *color,
+                      int64_t *n_out);
+
+/* dda_blocks / dda_blocks_batch (dda.py:8-86) on the device: rows grouped
+ * by segment in traversal order; batch_cap = 1 applies the batched
+ * variant's global lock-step cap.  *ray_ids / *coords are malloc'd
+ * (release with tsdf_free). */
+int tsdf_dda_blocks(const double *origins, const double *endpoints, int64_t n,
+                    double block_edge, int32_t batch_cap, int64_t **ray_ids, int64_t **coords,
+                    int64_t *nrows);
+/* select_merge_candidates (adapt.py:61-72): canonical-order coords of the
+ * level-0 blocks apply_merges would re-home; *coords malloc'd. */
+int tsdf_merge_candidates(tsdf_table *t, double sigma_threshold, double min_eligible_fraction,
+                          double min_mean_weight, int64_t **coords, int64_t *n_out);
+/* collapse_vertices (meshing.py:502-552) on the device */
+int tsdf_collapse_vertices(const double *vertices, const double *normals, const double *colors,
+                           int64_t nv, const int64_t *triangles, int64_t nt, double epsilon,
+                           tsdf_mesh *out);
+void tsdf_free(void *p);
+
+/* diagnostics */
+const char *tsdf_last_error(void);
+int64_t tsdf_kernel_launches(tsdf_table *t);
+int64_t tsdf_table_slots(tsdf_table *t);
+int tsdf_device_info(int32_t *sm_major, int32_t *sm_minor, int32_t *num_sms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSDF_B200_H */

@@ -1,0 +1,241 @@
+// extern "C" boundary (include/tsdf_b200.h) over the device implementation.
+#include <cstring>
+
+#include "../../include/tsdf_b200.h"
+#include "fusion.h"
+
+using namespace tsdf;
+
+struct tsdf_table {
+  Table* impl;
+};
+
+static inline Table* T_(tsdf_table* t) { return t ? t->impl : nullptr; }
+
+#define NEED(t)                               \
+  do {                                        \
+    if (!(t) || !(t)->impl) {                 \
+      set_error("null table handle");         \
+      return TSDF_EVALUE;                     \
+    }                                         \
+  } while (0)
+
+static Frame make_frame(const double* K, const double* R, const double* tr, double tau,
+                        double wcap) {
+  Frame f;
+  memset(&f, 0, sizeof(f));
+  if (K) {
+    f.fx = K[0];
+    f.fy = K[1];
+    f.cx = K[2];
+    f.cy = K[3];
+  }
+  memcpy(f.R, R, sizeof(f.R));
+  memcpy(f.t, tr, sizeof(f.t));
+  f.tau = tau;
+  f.weight_cap = wcap;
+  return f;
+}
+
+extern "C" {
+
+int tsdf_table_create(int64_t n_hash, int32_t bucket, int32_t overflow, double block_edge,
+                      int32_t n_levels, const int64_t* caps, void* stream, tsdf_table** out) {
+  *out = nullptr;
+  Table* impl = nullptr;
+  int s = table_create(n_hash, bucket, overflow, block_edge, n_levels, caps, stream, &impl);
+  if (s) return s;
+  *out = new tsdf_table{impl};
+  return TSDF_OK;
+}
+
+int tsdf_table_destroy(tsdf_table* t) {
+  if (!t) return TSDF_OK;
+  int s = table_destroy(t->impl);
+  delete t;
+  return s;
+}
+
+int tsdf_table_reset(tsdf_table* t) {
+  NEED(t);
+  return table_reset(T_(t));
+}
+
+int tsdf_table_set_shard(tsdf_table* t, int32_t rank, int32_t world) {
+  NEED(t);
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("invalid shard (rank, world)");
+    return TSDF_EVALUE;
+  }
+  T_(t)->d.shard_rank = rank;
+  T_(t)->d.shard_world = world;
+  return TSDF_OK;
+}
+
+int tsdf_integrate_depth(tsdf_table* t, const void* depth, int32_t depth_dtype, const void* rgb,
+                         int32_t rgb_dtype, int32_t height, int32_t width, int32_t mem,
+                         const double* K, const double* R, const double* trans, double tau,
+                         double weight_cap, tsdf_integration_stats* stats) {
+  NEED(t);
+  if (depth_dtype < 0 || depth_dtype > 3 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  if (K[0] <= 0 || K[1] <= 0) {
+    set_error("focal lengths must be positive");
+    return TSDF_EDATASET;
+  }
+  IntegrationStats st;
+  int s = integrate_depth(T_(t), depth, depth_dtype, rgb, rgb_dtype, height, width, mem,
+                          make_frame(K, R, trans, tau, weight_cap), &st);
+  memcpy(stats, &st, sizeof(st));
+  return s;
+}
+
+int tsdf_integrate_points(tsdf_table* t, const void* xyz, int32_t xyz_dtype, const void* rgb,
+                          int32_t rgb_dtype, int64_t n, int32_t mem, const double* R,
+                          const double* trans, double tau, double weight_cap,
+                          tsdf_integration_stats* stats) {
+  NEED(t);
+  if (xyz_dtype < 0 || xyz_dtype > 1 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  IntegrationStats st;
+  int s = integrate_points(T_(t), xyz, xyz_dtype, rgb, rgb_dtype, n, mem,
+                           make_frame(nullptr, R, trans, tau, weight_cap), &st);
+  memcpy(stats, &st, sizeof(st));
+  return s;
+}
+
+int tsdf_allocate_for_measurement(tsdf_table* t, const double* origin, const double* p,
+                                  double tau, int64_t* handles, int64_t max_out, int64_t* n_out) {
+  NEED(t);
+  return allocate_for_measurement(T_(t), origin, p, tau, handles, max_out, n_out);
+}
+
+int tsdf_apply_merges(tsdf_table* t, double sigma, double min_frac, double min_w,
+                      int32_t all_levels, tsdf_merge_stats* stats) {
+  NEED(t);
+  MergeStats st;
+  int s = apply_merges(T_(t), sigma, min_frac, min_w, all_levels, &st);
+  stats->candidates = st.candidates;
+  stats->merged = st.merged;
+  return s;
+}
+
+int tsdf_extract_mesh(tsdf_table* t, double iso, double eps, tsdf_mesh* out) {
+  NEED(t);
+  memset(out, 0, sizeof(*out));
+  if (eps < 0) eps = 0.25 * (T_(t)->d.edge / kFineSide);
+  MeshOut m{};
+  int s = extract_mesh(T_(t), iso, eps, &m);
+  out->vertices = m.v;
+  out->normals = m.n;
+  out->colors = m.c;
+  out->num_vertices = m.nv;
+  out->triangles = m.tri;
+  out->num_triangles = m.nt;
+  return s;
+}
+
+void tsdf_mesh_free(tsdf_mesh* m) {
+  if (!m) return;
+  MeshOut o{m->vertices, m->normals, m->colors, m->num_vertices, m->triangles, m->num_triangles};
+  mesh_free(&o);
+  memset(m, 0, sizeof(*m));
+}
+
+int tsdf_find_batch(tsdf_table* t, const int64_t* coords, int64_t n, int64_t* handles,
+                    int32_t* levels, uint8_t* found) {
+  NEED(t);
+  return find_batch(T_(t), coords, n, handles, levels, found);
+}
+
+int tsdf_insert(tsdf_table* t, const int64_t* coord, int32_t level, int64_t* handle) {
+  NEED(t);
+  return insert_block(T_(t), coord, level, handle);
+}
+
+int tsdf_remove(tsdf_table* t, const int64_t* coord, int32_t* level, double* tsdf,
+                double* weight, double* s2, float* color) {
+  NEED(t);
+  return remove_block(T_(t), coord, level, tsdf, weight, s2, color);
+}
+
+int tsdf_read_block(tsdf_table* t, const int64_t* coord, int32_t* level, double* tsdf,
+                    double* weight, double* s2, float* color) {
+  NEED(t);
+  return read_block(T_(t), coord, level, tsdf, weight, s2, color);
+}
+
+int tsdf_write_block(tsdf_table* t, const int64_t* coord, const double* tsdf,
+                     const double* weight, const double* s2, const float* color) {
+  NEED(t);
+  return write_block(T_(t), coord, tsdf, weight, s2, color);
+}
+
+int tsdf_live_count(tsdf_table* t, int32_t level, int64_t* n) {
+  NEED(t);
+  return live_count(T_(t), level, n);
+}
+
+int tsdf_export_level(tsdf_table* t, int32_t level, int64_t max_blocks, int64_t* coords,
+                      int64_t* handles, double* tsdf, double* weight, double* s2, float* color,
+                      int64_t* n_out) {
+  NEED(t);
+  return export_level(T_(t), level, max_blocks, coords, handles, tsdf, weight, s2, color, n_out);
+}
+
+const char* tsdf_last_error(void) { return last_error(); }
+
+int64_t tsdf_kernel_launches(tsdf_table* t) { return t && t->impl ? (int64_t)t->impl->launches : 0; }
+
+int64_t tsdf_table_slots(tsdf_table* t) { return t && t->impl ? (int64_t)t->impl->slots : 0; }
+
+int tsdf_device_info(int32_t* major, int32_t* minor, int32_t* sms) {
+  int dev = 0, n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_error("no CUDA device visible");
+    return TSDF_ECUDA;
+  }
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
+  return TSDF_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int tsdf_dda_blocks(const double* origins, const double* endpoints, int64_t n, double edge,
+                    int32_t batch_cap, int64_t** ray_ids, int64_t** coords, int64_t* nrows) {
+  return dda_trace(origins, endpoints, n, edge, batch_cap, ray_ids, coords, nrows);
+}
+
+int tsdf_merge_candidates(tsdf_table* t, double sigma, double min_frac, double min_w,
+                          int64_t** coords, int64_t* n_out) {
+  NEED(t);
+  return merge_candidates(T_(t), sigma, min_frac, min_w, coords, n_out);
+}
+
+int tsdf_collapse_vertices(const double* v, const double* n, const double* c, int64_t nv,
+                           const int64_t* tri, int64_t nt, double eps, tsdf_mesh* out) {
+  memset(out, 0, sizeof(*out));
+  MeshOut m{};
+  int s = collapse_vertices(v, n, c, nv, tri, nt, eps, &m);
+  out->vertices = m.v;
+  out->normals = m.n;
+  out->colors = m.c;
+  out->num_vertices = m.nv;
+  out->triangles = m.tri;
+  out->num_triangles = m.nt;
+  return s;
+}
+
+void tsdf_free(void* p) { free(p); }
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Host-side table object and the orchestration entry points behind the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "tsdf_common.cuh"
+
+namespace tsdf {
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Table {
+  DevTable d{};
+  uint32_t* free_top = nullptr;  // device [kMaxLevels]
+  int64_t caps[kMaxLevels] = {0, 0, 0, 0};
+  int32_t bucket = 0, overflow = 0;
+  uint64_t slots = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  Counters* dcnt = nullptr;  // device
+  Counters* hcnt = nullptr;  // pinned host mirror
+  uint32_t call_id = 0;
+  // scratch (grown on demand, never shrunk)
+  Buf in0, in1, dray, dcol, ends, flags, new_list, touched, work, pairs, pairs_alt, cub_tmp,
+      ray_len, ray_nhat, ray_src, ray_rgb, block_sums, lists, cand, mesh_scratch;
+  Buf cand_l[kMaxLevels];
+  // kernel launch telemetry: launches of our kernels since creation
+  uint64_t launches = 0;
+};
+
+struct IntegrationStats {
+  int64_t measurements, skipped_invalid, blocks_allocated, blocks_touched, voxels_updated,
+      observations;
+  int32_t no_valid_warning;
+  int32_t pad;
+};
+
+struct MergeStats {
+  int64_t candidates, merged;
+};
+
+struct Frame {
+  double fx, fy, cx, cy;
+  double R[9];
+  double t[3];
+  double tau, weight_cap;
+};
+
+void set_error(const std::string& msg);
+const char* last_error();
+int cuda_status(cudaError_t e, const char* where);
+void* grow(Buf& b, size_t bytes);
+
+int table_create(int64_t n_hash, int32_t bucket, int32_t overflow, double block_edge,
+                 int32_t n_levels, const int64_t* caps, void* stream, Table** out);
+int table_destroy(Table* t);
+int table_reset(Table* t);
+
+int integrate_depth(Table* T, const void* depth, int depth_dtype, const void* rgb,
+                    int rgb_dtype, int H, int W, int mem, const Frame& f,
+                    IntegrationStats* st);
+int integrate_points(Table* T, const void* xyz, int xyz_dtype, const void* rgb, int rgb_dtype,
+                     int64_t n, int mem, const Frame& f, IntegrationStats* st);
+int allocate_for_measurement(Table* T, const double* o, const double* p, double tau,
+                             int64_t* handles, int64_t max_out, int64_t* n_out);
+int apply_merges(Table* T, double sigma, double min_frac, double min_w, int all_levels,
+                 MergeStats* st);
+
+// block-level access (payloads, parity export)
+int find_batch(Table* T, const int64_t* coords, int64_t n, int64_t* handles, int32_t* levels,
+               uint8_t* found);
+int insert_block(Table* T, const int64_t* coord, int32_t level, int64_t* handle);
+int remove_block(Table* T, const int64_t* coord, int32_t* level, double* tsdf, double* weight,
+                 double* s2, float* color);
+int read_block(Table* T, const int64_t* coord, int32_t* level, double* tsdf, double* weight,
+               double* s2, float* color);
+int write_block(Table* T, const int64_t* coord, const double* tsdf, const double* weight,
+                const double* s2, const float* color);
+int live_count(Table* T, int32_t level, int64_t* n);
+int export_level(Table* T, int32_t level, int64_t max_blocks, int64_t* coords, int64_t* handles,
+                 double* tsdf, double* weight, double* s2, float* color, int64_t* n_out);
+
+struct MeshOut {
+  double *v, *n, *c;
+  int64_t nv;
+  int64_t* tri;
+  int64_t nt;
+};
+
+int dda_trace(const double* origins, const double* endpoints, int64_t n, double edge, int capped,
+              int64_t** ray_ids, int64_t** coords, int64_t* nrows);
+int merge_candidates(Table* T, double sigma, double min_frac, double min_w, int64_t** coords,
+                     int64_t* n_out);
+int collapse_vertices(const double* v, const double* n, const double* c, int64_t nv,
+                      const int64_t* tri, int64_t nt, double eps, MeshOut* out);
+
+// mesh extraction (mesh.cu)
+int extract_mesh(Table* T, double iso, double eps, MeshOut* out);
+void mesh_free(MeshOut* m);
+
+}  // namespace tsdf

@@ -1,0 +1,268 @@
+"""Device-resident flat spatial hash over voxel blocks of several resolutions.
+
+Drop-in for the reference's ``HashTable`` (hashgrid.py:139-354): the same
+constructor, find / insert / remove / find_batch / insert_batch /
+live_blocks, per-level heaps and capacity semantics (level heaps plus the
+bucket + overflow-chain limit per Teschner slot, emulated with per-slot
+occupancy counters).  The index itself is an open-addressing table of
+64-bit packed keys in HBM with lock-free atomicCAS insertion
+(csrc/tsdf_common.cuh); voxel payloads live in per-level SoA slabs on the
+device.  ``heaps[level].tsdf`` etc. are read-only host snapshots indexed by
+heap handle, like the reference's arrays; write voxel data with
+``write_payload``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import CapacityError, NotFoundError
+
+HASH_PRIMES = (73856093, 19349669, 83492791)
+FINE_SIDE = 8
+_M64 = 1 << 64
+
+
+def hash_key(coord, n_hash: int) -> int:
+    """Reference slot index (hashgrid.py:30-46): 64-bit wrapped Teschner hash,
+    Euclidean mod."""
+    if n_hash <= 0:
+        raise ValueError("n_hash must be positive")
+    x, y, z = (int(c) for c in coord)
+    h = ((x * HASH_PRIMES[0]) ^ (y * HASH_PRIMES[1]) ^ (z * HASH_PRIMES[2])) & (_M64 - 1)
+    if h >= 1 << 63:
+        h -= _M64
+    return h % n_hash
+
+
+def hash_key_batch(coords, n_hash: int) -> np.ndarray:
+    c = np.asarray(coords, dtype=np.int64).reshape(-1, 3)
+    with np.errstate(over="ignore"):
+        h = (c[:, 0] * np.int64(HASH_PRIMES[0])) ^ (c[:, 1] * np.int64(HASH_PRIMES[1])) \
+            ^ (c[:, 2] * np.int64(HASH_PRIMES[2]))
+    return h % np.int64(n_hash)
+
+
+def voxel_side(level: int) -> int:
+    return FINE_SIDE >> level
+
+
+def voxel_count(level: int) -> int:
+    return voxel_side(level) ** 3
+
+
+def voxel_index(world_point, block_coord, level: int, block_edge: float) -> int:
+    """Row-major (x slowest, z fastest) voxel offset of a point in a block
+    (hashgrid.py:357-367)."""
+    p = np.asarray(world_point, dtype=np.float64)
+    local = p - np.asarray(block_coord, dtype=np.float64) * block_edge
+    if np.any(local < 0) or np.any(local >= block_edge):
+        raise ValueError(f"point {tuple(p)} lies outside block {tuple(block_coord)}")
+    side = voxel_side(level)
+    ijk = np.minimum((local / (block_edge / side)).astype(np.int64), side - 1)
+    return int((ijk[0] * side + ijk[1]) * side + ijk[2])
+
+
+@dataclass
+class BlockPayload:
+    """Full copy of one block's voxel data, detached from the table."""
+
+    coord: tuple
+    level: int
+    tsdf: np.ndarray
+    weight: np.ndarray
+    s2: np.ndarray
+    color: np.ndarray
+
+
+class BlockHeap:
+    """Per-level view: sizes, occupancy and read-only snapshots by handle."""
+
+    def __init__(self, table: "HashTable", level: int, capacity: int):
+        self._table = table
+        self.level = level
+        self.side = voxel_side(level)
+        self.nvox = self.side ** 3
+        self.capacity = int(capacity)
+
+    @property
+    def occupied(self) -> int:
+        n = C.c_int64()
+        N.check(N.lib().tsdf_live_count(self._table._h, self.level, C.byref(n)), "live_count")
+        return int(n.value)
+
+    def fill_fraction(self) -> float:
+        return self.occupied / self.capacity if self.capacity else 0.0
+
+    def _snapshot(self):
+        coords, handles, t, w, s2, c = self._table.export_level(self.level)
+        n = self.capacity * self.nvox
+        out = {"tsdf": np.zeros(n), "weight": np.zeros(n), "s2": np.zeros(n),
+               "color": np.zeros((n, 3), dtype=np.float32),
+               "coords": np.zeros((self.capacity, 3), dtype=np.int64),
+               "live": np.zeros(self.capacity, dtype=bool)}
+        if len(handles):
+            idx = (handles[:, None] * self.nvox + np.arange(self.nvox)).ravel()
+            out["tsdf"][idx] = t.ravel()
+            out["weight"][idx] = w.ravel()
+            out["s2"][idx] = s2.ravel()
+            out["color"][idx] = c.reshape(-1, 3)
+            out["coords"][handles] = coords
+            out["live"][handles] = True
+        for a in out.values():
+            a.setflags(write=False)
+        return out
+
+    def __getattr__(self, name):
+        if name in ("tsdf", "weight", "s2", "color", "coords", "live"):
+            return self._snapshot()[name]
+        raise AttributeError(name)
+
+
+class HashTable:
+    """Index from integer block coordinates to (heap handle, level)."""
+
+    def __init__(self, n_hash: int, bucket_capacity: int, overflow_capacity: int,
+                 block_edge: float, heap_capacities=(16384, 8192), stream=None):
+        if n_hash <= 0 or bucket_capacity <= 0 or overflow_capacity <= 0:
+            raise ValueError("table sizes must be positive")
+        self.n_hash = int(n_hash)
+        self.bucket_capacity = int(bucket_capacity)
+        self.overflow_capacity = int(overflow_capacity)
+        self.block_edge = float(block_edge)
+        caps = np.ascontiguousarray([int(c) for c in heap_capacities], dtype=np.int64)
+        h = C.c_void_p()
+        stream_ptr = None if stream is None else int(getattr(stream, "cuda_stream", stream))
+        N.check(N.lib().tsdf_table_create(self.n_hash, self.bucket_capacity,
+                                          self.overflow_capacity, self.block_edge, len(caps),
+                                          caps, stream_ptr, C.byref(h)), "HashTable")
+        self._h = h
+        self.heaps = [BlockHeap(self, l, c) for l, c in enumerate(caps.tolist())]
+        self.num_levels = len(self.heaps)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().tsdf_table_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- sizes -----------------------------------------------------------
+    def voxel_size(self, level: int) -> float:
+        return self.block_edge / voxel_side(level)
+
+    def live_count(self) -> int:
+        return sum(h.occupied for h in self.heaps)
+
+    def fill_fractions(self) -> list:
+        return [h.fill_fraction() for h in self.heaps]
+
+    def set_shard(self, rank: int, world: int) -> None:
+        """Own only blocks whose key hashes to ``rank`` of ``world`` GPUs."""
+        N.check(N.lib().tsdf_table_set_shard(self._h, int(rank), int(world)), "set_shard")
+
+    def reset(self) -> None:
+        N.check(N.lib().tsdf_table_reset(self._h), "reset")
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(N.lib().tsdf_kernel_launches(self._h))
+
+    # -- core operations ---------------------------------------------------
+    def find(self, coord):
+        h, l, f = self.find_batch(np.asarray(coord, dtype=np.int64).reshape(1, 3))
+        return (int(h[0]), int(l[0])) if f[0] else None
+
+    def insert(self, coord, level: int) -> int:
+        out = C.c_int64()
+        N.check(N.lib().tsdf_insert(self._h, np.asarray(coord, dtype=np.int64).reshape(3),
+                                    int(level), C.byref(out)), "insert")
+        return int(out.value)
+
+    def _payload_call(self, fn, coord, what):
+        c = np.asarray(coord, dtype=np.int64).reshape(3)
+        found = self.find(c)
+        if found is None:
+            raise NotFoundError(f"block {tuple(int(v) for v in c)} is not live")
+        nvox = self.heaps[found[1]].nvox
+        t, w, s2 = np.zeros(nvox), np.zeros(nvox), np.zeros(nvox)
+        col = np.zeros((nvox, 3), dtype=np.float32)
+        lv = C.c_int32()
+        N.check(fn(self._h, c, C.byref(lv), t.ctypes.data, w.ctypes.data, s2.ctypes.data,
+                   col.ctypes.data), what)
+        return BlockPayload(coord=tuple(int(v) for v in c), level=int(lv.value), tsdf=t,
+                            weight=w, s2=s2, color=col)
+
+    def remove(self, coord) -> BlockPayload:
+        return self._payload_call(N.lib().tsdf_remove, coord, "remove")
+
+    def payload(self, coord) -> BlockPayload:
+        return self._payload_call(N.lib().tsdf_read_block, coord, "payload")
+
+    def write_payload(self, coord, payload: BlockPayload) -> None:
+        c = np.asarray(coord, dtype=np.int64).reshape(3)
+        t = np.ascontiguousarray(payload.tsdf, dtype=np.float64)
+        w = np.ascontiguousarray(payload.weight, dtype=np.float64)
+        s2 = np.ascontiguousarray(payload.s2, dtype=np.float64)
+        col = np.ascontiguousarray(payload.color, dtype=np.float32)
+        N.check(N.lib().tsdf_write_block(self._h, c, t.ctypes.data, w.ctypes.data,
+                                         s2.ctypes.data, col.ctypes.data), "write_payload")
+
+    # -- batch operations ------------------------------------------------------
+    def find_batch(self, coords):
+        c = np.ascontiguousarray(np.asarray(coords, dtype=np.int64).reshape(-1, 3))
+        n = len(c)
+        handles = np.full(n, -1, dtype=np.int64)
+        levels = np.zeros(n, dtype=np.int32)
+        found = np.zeros(n, dtype=np.uint8)
+        if n:
+            N.check(N.lib().tsdf_find_batch(self._h, c, n, handles, levels, found), "find_batch")
+        return handles, levels.astype(np.int64), found.astype(bool)
+
+    def insert_batch(self, coords, level: int):
+        c = np.asarray(coords, dtype=np.int64).reshape(-1, 3)
+        handles, levels, found = self.find_batch(c)
+        created = ~found
+        for j in np.nonzero(created)[0]:
+            handles[j] = self.insert(c[j], level)
+            levels[j] = level
+        return handles, levels, created
+
+    # -- iteration ---------------------------------------------------------
+    def export_level(self, level: int):
+        """(coords, handles, tsdf, weight, s2, color) of every live block of a
+        level in canonical (x, y, z) order."""
+        n = C.c_int64()
+        N.check(N.lib().tsdf_export_level(self._h, int(level), 0, None, None, None, None, None,
+                                          None, C.byref(n)), "export_level")
+        nb, nvox = int(n.value), self.heaps[level].nvox
+        coords = np.zeros((nb, 3), dtype=np.int64)
+        handles = np.zeros(nb, dtype=np.int64)
+        t, w, s2 = (np.zeros((nb, nvox)) for _ in range(3))
+        col = np.zeros((nb, nvox, 3), dtype=np.float32)
+        if nb:
+            N.check(N.lib().tsdf_export_level(self._h, int(level), nb, coords.ctypes.data,
+                                              handles.ctypes.data, t.ctypes.data, w.ctypes.data,
+                                              s2.ctypes.data, col.ctypes.data, C.byref(n)),
+                    "export_level")
+        return coords, handles, t, w, s2, col
+
+    def live_blocks(self, level: int, sort: bool = True):
+        coords, handles, *_ = self.export_level(level)
+        return coords, handles
+
+    def key_levels(self) -> dict:
+        """{coord: level} of every live block (the parity key set)."""
+        out = {}
+        for l in range(self.num_levels):
+            for c in map(tuple, self.live_blocks(l)[0].tolist()):
+                out[c] = l
+        return out

@@ -1,0 +1,153 @@
+"""Fusion of depth frames and point clouds into the device-resident grid.
+
+``integrate_depth`` / ``integrate_pointcloud`` / ``allocate_for_measurement``
+keep the reference signatures (integrate.py:143-342) and run entirely on
+the GPU: frame prep, full-ray FP64 DDA with lock-free block allocation,
+touched-block compaction and the per-voxel Welford update
+(csrc/fusion.cu).  The scalar helpers (``sdf_ray``, ``sdf_projective``,
+``update_voxel``, ``Voxel``) are the reference's single-value formulas,
+kept for API parity; they are not on the integration path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .geometry import DepthFrame, PointCloudFrame
+from .hashgrid import HashTable
+
+
+@dataclass
+class Voxel:
+    tsdf: float = 0.0
+    weight: float = 0.0
+    color: tuple = (0.0, 0.0, 0.0)
+    s2: float = 0.0
+
+    def variance(self) -> float:
+        return self.s2 / self.weight if self.weight >= 1 else 0.0
+
+
+@dataclass
+class IntegrationStats:
+    measurements: int = 0
+    skipped_invalid: int = 0
+    blocks_allocated: int = 0
+    blocks_touched: int = 0
+    voxels_updated: int = 0
+    observations: int = 0
+    warnings: list = field(default_factory=list)
+
+
+def sdf_ray(p, x, o, tau: float) -> float:
+    """Along-ray signed distance of x to surface point p, clipped (integrate.py:53-65)."""
+    p, x, o = (np.asarray(v, dtype=np.float64) for v in (p, x, o))
+    ray = p - o
+    n = np.linalg.norm(ray)
+    if n == 0.0:
+        raise ValueError("surface point coincides with the sensor origin")
+    return float(np.clip(np.dot(p - x, ray / n), -tau, tau))
+
+
+def sdf_projective(d: float, x, tau: float) -> float:
+    """Measured ray distance minus voxel range, clipped (integrate.py:68-71)."""
+    return float(np.clip(d - np.linalg.norm(np.asarray(x, dtype=np.float64)), -tau, tau))
+
+
+def update_voxel(v: Voxel, d_k: float, rgb=None, weight_cap: float = 0.0) -> Voxel:
+    """One unit-weight running-mean + Welford step (integrate.py:74-89)."""
+    w0 = v.weight
+    mean = (w0 * v.tsdf + d_k) / (w0 + 1.0)
+    s2 = v.s2 + (d_k - v.tsdf) * (d_k - mean)
+    w1 = w0 + 1.0
+    if weight_cap > 0.0:
+        w1 = min(w1, weight_cap)
+    color = v.color
+    if rgb is not None:
+        color = tuple((w0 * np.asarray(v.color) + np.asarray(rgb)) / (w0 + 1.0))
+    return Voxel(tsdf=mean, weight=w1, color=color, s2=s2)
+
+
+def _check_archive(archive):
+    if archive is not None and len(archive) != 0:
+        raise NotImplementedError("the streaming / archive tier is outside this build's scope")
+
+
+def _stats(st) -> IntegrationStats:
+    out = IntegrationStats(st.measurements, st.skipped_invalid, st.blocks_allocated,
+                           st.blocks_touched, st.voxels_updated, st.observations)
+    if st.no_valid_warning:
+        out.warnings.append("frame has no valid depth pixels")
+    return out
+
+
+def _pose(pose):
+    return (np.ascontiguousarray(pose.rotation, dtype=np.float64).reshape(9),
+            np.ascontiguousarray(pose.translation, dtype=np.float64).reshape(3))
+
+
+def integrate_depth(table: HashTable, frame: DepthFrame, tau: float, archive=None,
+                    weight_cap: float = 0.0) -> IntegrationStats:
+    """Projective fusion of one depth image (integrate.py:255-342)."""
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    _check_archive(archive)
+    dptr, ddt, dmem, _keep_d = N.as_buffer(frame.depth, (N.F64, N.F32))
+    cptr, cdt, cmem, _keep_c = (None, 0, dmem, None)
+    if frame.color is not None:
+        cptr, cdt, cmem, _keep_c = N.as_buffer(frame.color, (N.F64, N.F32, N.U8))
+        if cmem != dmem:
+            raise ValueError("depth and colour must both live on the host or both on the device")
+    R, t = _pose(frame.pose)
+    st = N.IntegrationStatsC()
+    N.check(N.lib().tsdf_integrate_depth(table._h, dptr, ddt, cptr, cdt, frame.height,
+                                         frame.width, dmem, frame.intrinsics.as_array(), R, t,
+                                         float(tau), float(weight_cap), C.byref(st)),
+            "integrate_depth")
+    return _stats(st)
+
+
+def integrate_pointcloud(table: HashTable, frame: PointCloudFrame, tau: float, archive=None,
+                         weight_cap: float = 0.0) -> IntegrationStats:
+    """Ray-based fusion of one point cloud (integrate.py:175-252)."""
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    _check_archive(archive)
+    n = int(frame.points.shape[0])
+    if n == 0:
+        return IntegrationStats()
+    pptr, pdt, pmem, _keep_p = N.as_buffer(frame.points, (N.F64, N.F32))
+    cptr, cdt, _keep_c = None, 0, None
+    if frame.colors is not None:
+        cptr, cdt, cmem, _keep_c = N.as_buffer(frame.colors, (N.F64, N.F32, N.U8))
+        if cmem != pmem:
+            raise ValueError("points and colours must both live on the host or both on the device")
+    R, t = _pose(frame.pose)
+    st = N.IntegrationStatsC()
+    N.check(N.lib().tsdf_integrate_points(table._h, pptr, pdt, cptr, cdt, n, pmem, R, t,
+                                          float(tau), float(weight_cap), C.byref(st)),
+            "integrate_pointcloud")
+    return _stats(st)
+
+
+def allocate_for_measurement(table: HashTable, origin, p, tau: float, archive=None) -> list:
+    """Allocate every block the segment origin -> p (+tau) crosses
+    (integrate.py:143-161); handles in traversal order."""
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    _check_archive(archive)
+    o = np.ascontiguousarray(origin, dtype=np.float64).reshape(3)
+    q = np.ascontiguousarray(p, dtype=np.float64).reshape(3)
+    cap = 1 << 16
+    out = np.zeros(cap, dtype=np.int64)
+    n = C.c_int64()
+    N.check(N.lib().tsdf_allocate_for_measurement(table._h, o, q, float(tau), out, cap,
+                                                  C.byref(n)), "allocate_for_measurement")
+    if n.value > cap:
+        out = np.zeros(n.value, dtype=np.int64)
+        N.check(N.lib().tsdf_allocate_for_measurement(table._h, o, q, float(tau), out, n.value,
+                                                      C.byref(n)), "allocate_for_measurement")
+    return [int(h) for h in out[:n.value]]
