@@ -1,0 +1,403 @@
+"""Benchmark of the B200 TSDF-fusion hot path (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 2 -- synthetic indoor room, 640x480 RGB-D
+(f32 depth + u8 RGB, 7 B/px), 3 resolution levels 5/10/20 mm (labelled
+multi-level merge extension), the SURVEY §8d "large room" (6 x 5 x 3 m,
+12 spheres) swept by the reference's yaw/pitch trajectory over 500 frames.
+One step = one merge window: 10 frames integrated + one merge pass
+(merge_cadence = 10).  value = integrated Mpoints/s (valid depth pixels /
+device time), inputs resident in HBM; e2e = the same through the public
+API from pinned host buffers (H2D inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload room|lidar]
+
+Multi-GPU (torchrun, one rank per GPU): block-key-hash sharding -- every
+rank integrates the same frames and owns 1/N of the blocks (strong
+scaling of a fixed frame stream); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "room": dict(kind="depth", scene="large_room", width=640, height=480, edge=0.04, tau=0.015,
+                 sigma=2.5e-5, caps=(1_500_000, 300_000, 100_000), n_hash=4_000_037,
+                 cadence=10, frames_total=500,
+                 name="large room 6x5x3 m, 640x480 RGB-D (f32 depth + u8 RGB), 3 levels 5/10/20 mm, "
+                      "500-frame sweep, merge every 10 frames"),
+    "lidar": dict(kind="lidar", beams=128, columns=2048, edge=1.6, tau=0.8, sigma=1e-2,
+                  caps=(1_500_000, 200_000, 50_000), n_hash=4_000_037, cadence=10, step_m=0.5,
+                  name="128-beam x 2048-column LiDAR, 100 m range, 0.2/0.4/0.8 m levels, "
+                       "sensor advancing 0.5 m/scan, merge every 10 scans"),
+}
+FRAMES_PER_STEP = 10
+S_IN = {"depth": 7, "lidar": 12}  # algorithmic input bytes per measurement
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_frames(wl, n, start=0):
+    from paper_2511_21459_b200 import synth
+    if wl["kind"] == "depth":
+        scene = synth.make_scene(wl["scene"])
+        intr = synth.default_intrinsics("room", wl["width"], wl["height"])
+        poses = synth.trajectory(synth.Scene("room"), wl["frames_total"])
+        out = []
+        for i in range(start, start + n):
+            d, c = synth.render_depth(scene, poses[i % len(poses)], intr, wl["width"], wl["height"])
+            out.append((d.astype(np.float32), np.round(c * 255.0).astype(np.uint8),
+                        poses[i % len(poses)], intr))
+        return out
+    scene = synth.make_lidar_scene()
+    dirs = synth.lidar_directions(wl["beams"], wl["columns"])
+    from paper_2511_21459_b200.geometry import SensorPose
+    out = []
+    for i in range(start, start + n):
+        org = np.array([wl["step_m"] * i, 0.0, 0.0])
+        out.append((synth.lidar_scan(scene, org, dirs), None, SensorPose(np.eye(3), org), None))
+    return out
+
+
+def n_meas(fr):
+    d = fr[0]
+    return int(np.count_nonzero(np.isfinite(d) & (d > 0))) if d.ndim == 2 else int(len(d))
+
+
+def make_table(P, wl, stream=None, shard=None):
+    t = P.HashTable(wl["n_hash"], 10, 7, wl["edge"], wl["caps"], stream=stream)
+    if shard:
+        t.set_shard(*shard)
+    return t
+
+
+def integrate(P, t, wl, fr, device=None):
+    d, c, pose, intr = fr
+    if wl["kind"] == "depth":
+        f = P.DepthFrame(depth=d if device is None else device[0], intrinsics=intr, pose=pose,
+                         color=c if device is None else device[1])
+        return P.integrate_depth(t, f, wl["tau"])
+    f = P.PointCloudFrame(points=d if device is None else device[0], pose=pose)
+    return P.integrate_pointcloud(t, f, wl["tau"])
+
+
+def kernel_bytes(stats_list, wl):
+    """Algorithmic bytes: B = s_in*P + 16*T + 16*A + 48*U per frame."""
+    s_in = S_IN[wl["kind"]]
+    P_ = sum(s.measurements for s in stats_list)
+    T_ = sum(s.blocks_touched for s in stats_list)
+    A_ = sum(s.blocks_allocated for s in stats_list)
+    U_ = sum(s.voxels_updated for s in stats_list)
+    return {"path": s_in * P_ + 16 * T_ + 16 * A_ + 48 * U_,
+            "update": 48 * U_ + 16 * T_,          # voxel RMW + hash-entry reads
+            "alloc": s_in * P_ + 16 * T_ + 16 * A_,  # frame read + entry probes/writes
+            "P": P_, "T": T_, "A": A_, "U": U_}
+
+
+KERNEL_ROLE = {"k_depth_update": "update", "k_lidar_update": "update", "k_dda_walk": "alloc"}
+
+
+def run_b200(args, wl, rank, world, dist, torch):
+    import paper_2511_21459_b200 as P
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    shard = (rank, world) if world > 1 else None
+    W, K = args.warmup, args.steps
+    nfr = FRAMES_PER_STEP * (W + K)
+    t0 = time.time()
+    frames = make_frames(wl, nfr)
+    log(f"[bench] generated {nfr} frames in {time.time() - t0:.1f}s")
+    # device-resident inputs
+    dframes = []
+    for d, c, _, _ in frames:
+        dframes.append((torch.from_numpy(d).to(dev), None if c is None else torch.from_numpy(c).to(dev)))
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # 256 MB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- value: inputs resident in HBM -----------------------------------
+    with torch.cuda.stream(stream):
+        table = make_table(P, wl, stream=stream, shard=shard)
+    all_stats, step_ms, merged = [], [], 0
+    fi = 0
+    for s in range(W):
+        for _ in range(FRAMES_PER_STEP):
+            integrate(P, table, wl, frames[fi], dframes[fi])
+            fi += 1
+        P.apply_merges(table, wl["sigma"], all_levels=True)
+    table.profile(True)
+    table.kernel_times(reset=True)
+    launches0 = table.kernel_launches
+    barrier()
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    with sampler:
+        for s in range(K):
+            flush.fill_(s & 0xFF)  # L2 flush between timed steps (outside the events)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(FRAMES_PER_STEP):
+                all_stats.append(integrate(P, table, wl, frames[fi], dframes[fi]))
+                fi += 1
+            merged += P.apply_merges(table, wl["sigma"], all_levels=True).merged
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    barrier()
+    launches = table.kernel_launches - launches0
+    ktimes = table.kernel_times(reset=True)
+    table.profile(False)
+    occ = [h.occupied for h in table.heaps]
+    dev_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms = float(tt.item())
+    points = sum(s.measurements for s in all_stats)  # invariant across ranks
+    nframes = K * FRAMES_PER_STEP
+    value = points / (dev_ms * 1e-3) / 1e6
+    fps = nframes / (dev_ms * 1e-3)
+    table.close()
+    del table
+
+    # ---- e2e: public API from pinned host buffers ----------------------------
+    with torch.cuda.stream(stream):
+        t2 = make_table(P, wl, stream=stream, shard=shard)
+    pinned = []
+    for d, c, pose, intr in frames:
+        pd = torch.from_numpy(d).pin_memory().numpy()
+        pc = None if c is None else torch.from_numpy(c).pin_memory().numpy()
+        pinned.append((pd, pc, pose, intr))
+    h2d = d2h = 0
+    fi = 0
+    for s in range(W):
+        for _ in range(FRAMES_PER_STEP):
+            integrate(P, t2, wl, pinned[fi])
+            fi += 1
+        P.apply_merges(t2, wl["sigma"], all_levels=True)
+    barrier()
+    e2e_t0 = time.perf_counter()
+    e2e_pts = 0
+    for s in range(K):
+        for _ in range(FRAMES_PER_STEP):
+            fr = pinned[fi]
+            st = integrate(P, t2, wl, fr)
+            e2e_pts += st.measurements
+            h2d += fr[0].nbytes + (0 if fr[1] is None else fr[1].nbytes)
+            d2h += 256  # per-call counters block (stats) read back
+            fi += 1
+        P.apply_merges(t2, wl["sigma"], all_levels=True)
+        d2h += 256
+    barrier()
+    e2e_s = time.perf_counter() - e2e_t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    t2.close()
+    e2e_value = e2e_pts / e2e_s / 1e6
+
+    # ---- roofline of the dominant kernel (live CUDA-event durations) ---------
+    peak, peak_kind = peaks()
+    B = kernel_bytes(all_stats, wl)
+    top = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else ("none", (0.0, 1))
+    top_name, (top_ms, top_n) = top
+    role = KERNEL_ROLE.get(top_name, "path")
+    top_bytes = B[role] if role in B else B["path"]
+    achieved = (top_bytes / top_n) / ((top_ms / top_n) * 1e-3) / 1e9 if top_ms > 0 else 0.0
+    path_gbs = B["path"] / (dev_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("traffic_per_launch", {}).get(top_name)
+        except Exception:
+            traffic = None
+    out = {
+        "metric": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)" if wl["kind"] == "depth"
+                  else "integrated Mpoints/s (128-beam LiDAR)",
+        "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": round(dev_ms / K, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic ray-cast scene, deterministic)",
+        "config": {"workload": wl["name"], "frames_per_step": FRAMES_PER_STEP,
+                   "fps": round(fps, 2), "frames_timed": nframes,
+                   "l2": "256 MB L2 flush between timed steps (outside the events)",
+                   "parallelism": f"block-key-hash shards x{world}" if world > 1 else "single GPU",
+                   "blocks_live_end": occ, "merged_in_timed_region": merged,
+                   "work_units": {k: int(v) for k, v in B.items() if k in "PTAU"}},
+        "e2e": {"value": round(e2e_value, 3), "unit": "Mpoints/s", "h2d_bytes_per_step": h2d // K,
+                "d2h_bytes_per_step": d2h // K},
+        "roofline": {"bound": "hbm", "kernel": top_name, "achieved": round(achieved, 2),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 5),
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "path_achieved_gbs": round(path_gbs, 2),
+                     "path_frac": round(path_gbs / peak, 5),
+                     "bytes_per_launch": round(top_bytes / max(top_n, 1)),
+                     "ms_per_launch": round(top_ms / max(top_n, 1), 4)},
+        "kernels_ms": {k: [round(v[0], 3), v[1]] for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])},
+        "gpu_launches": int(launches),
+        "clocks": sampler.summary(),
+    }
+    return out
+
+
+def run_oracle_frames(wl, frames):
+    """The oracle port on the host (cpu_baseline / reference arm)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle.oracle import OracleTable
+    # heaps sized for the bounded sample (calloc'd pages are only committed on touch)
+    t = OracleTable(wl["n_hash"], 10, 7, wl["edge"], (600_000, 40_000, 10_000))
+    pts, secs = 0, []
+    for d, c, pose, intr in frames:
+        t0 = time.perf_counter()
+        if wl["kind"] == "depth":
+            st = t.integrate_depth(d.astype(np.float64), [intr.fx, intr.fy, intr.cx, intr.cy],
+                                   pose.rotation, pose.translation, wl["tau"],
+                                   color=c.astype(np.float64) / 255.0)
+        else:
+            st = t.integrate_points(d.astype(np.float64), pose.rotation, pose.translation, wl["tau"])
+        secs.append(time.perf_counter() - t0)
+        pts += st["measurements"]
+    return pts, secs
+
+
+def cpu_baseline(wl, n_frames=2):
+    frames = make_frames(wl, n_frames)
+    pts, secs = run_oracle_frames(wl, frames)
+    return {"value": round(pts / sum(secs) / 1e6, 4), "unit": "Mpoints/s", "cores": 1,
+            "kind": "port",
+            "sample": f"first {n_frames} frames of the same workload through the C oracle "
+                      f"(oracle/tsdf_oracle.c, serial, -O2), {sum(secs):.1f} s"}
+
+
+def run_reference(args, wl):
+    frames = make_frames(wl, args.warmup + args.steps)
+    pts, secs = run_oracle_frames(wl, frames)
+    tp = sum(secs[args.warmup:])
+    ppts = sum(n_meas(f) for f in frames[args.warmup:])
+    v = ppts / tp / 1e6
+    return {"impl": "reference", "metric": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)"
+            if wl["kind"] == "depth" else "integrated Mpoints/s (128-beam LiDAR)",
+            "value": round(v, 4), "unit": "Mpoints/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(tp / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic ray-cast scene, deterministic)",
+            "config": {"workload": wl["name"], "frames_per_step": 1,
+                       "note": "reference arm = the oracle port of the reference algorithm on the "
+                               "host CPU (the reference is pure NumPy; same arithmetic, serial C)"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "Mpoints/s", "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} timed frames after {args.warmup} warm-up"},
+            "e2e": {"value": round(v, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="room", choices=list(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    wl = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, wl)), flush=True)
+        return
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    out = run_b200(args, wl, rank, world, dist, torch)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(wl)
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

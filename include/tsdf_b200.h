@@ -161,6 +161,12 @@ int tsdf_collapse_vertices(const double *vertices, const double *normals, const 
 void tsdf_free(void *p);
 
 /* diagnostics */
+/* per-kernel device time: CUDA events bracket every launch on the table's
+ * stream while enabled; tsdf_profile_read returns {name, total ms, launches}
+ * per kernel (names: name_stride bytes each). */
+int tsdf_profile_enable(tsdf_table *t, int32_t on);
+int tsdf_profile_read(tsdf_table *t, int32_t reset, int32_t max_entries, char *names,
+                      int32_t name_stride, double *ms, int64_t *counts, int32_t *n_out);
 const char *tsdf_last_error(void);
 int64_t tsdf_kernel_launches(tsdf_table *t);
 int64_t tsdf_table_slots(tsdf_table *t);

@@ -239,3 +239,36 @@ int tsdf_collapse_vertices(const double* v, const double* n, const double* c, in
 void tsdf_free(void* p) { free(p); }
 
 }  // extern "C"
+
+extern "C" {
+
+int tsdf_profile_enable(tsdf_table* t, int32_t on) {
+  NEED(t);
+  T_(t)->prof = on != 0;
+  if (!on) {
+    prof_collect(T_(t));
+  }
+  return TSDF_OK;
+}
+
+int tsdf_profile_read(tsdf_table* t, int32_t reset, int32_t max_entries, char* names,
+                      int32_t name_stride, double* ms, int64_t* counts, int32_t* n_out) {
+  NEED(t);
+  Table* T = T_(t);
+  if (int s = prof_collect(T)) return s;
+  int i = 0;
+  for (const auto& kv : T->prof_acc) {
+    if (i < max_entries) {
+      strncpy(names + (size_t)i * name_stride, kv.first.c_str(), name_stride - 1);
+      names[(size_t)i * name_stride + name_stride - 1] = 0;
+      ms[i] = kv.second.ms;
+      counts[i] = kv.second.count;
+    }
+    i++;
+  }
+  *n_out = i;
+  if (reset) T->prof_acc.clear();
+  return TSDF_OK;
+}
+
+}  // extern "C"

@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <vector>
 
 #include "tsdf_common.cuh"
 
@@ -12,6 +14,15 @@ namespace tsdf {
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
+};
+
+struct ProfRec {
+  const char* name;
+  cudaEvent_t start, stop;
+};
+struct ProfAcc {
+  double ms = 0;
+  int64_t count = 0;
 };
 
 struct Table {
@@ -31,7 +42,17 @@ struct Table {
   Buf cand_l[kMaxLevels];
   // kernel launch telemetry: launches of our kernels since creation
   uint64_t launches = 0;
+  // optional per-kernel event timing (bench / profiling)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
+  std::vector<ProfRec> prof_recs;
+  std::map<std::string, ProfAcc> prof_acc;
 };
+
+int prof_begin(Table* T, const char* name);
+void prof_end(Table* T, int id);
+int prof_collect(Table* T);
 
 struct IntegrationStats {
   int64_t measurements, skipped_invalid, blocks_allocated, blocks_touched, voxels_updated,

@@ -172,6 +172,26 @@ class HashTable:
     def reset(self) -> None:
         N.check(N.lib().tsdf_table_reset(self._h), "reset")
 
+    def profile(self, on: bool = True) -> None:
+        """Bracket every kernel launch with CUDA events on the table's stream."""
+        N.check(N.lib().tsdf_profile_enable(self._h, int(bool(on))), "profile")
+
+    def kernel_times(self, reset: bool = True) -> dict:
+        """{kernel: (total ms, launches)} accumulated while profiling."""
+        cap, stride = 64, 64
+        names = C.create_string_buffer(cap * stride)
+        ms = np.zeros(cap)
+        cnt = np.zeros(cap, dtype=np.int64)
+        n = C.c_int32()
+        N.check(N.lib().tsdf_profile_read(self._h, int(reset), cap, names, stride, ms, cnt,
+                                          C.byref(n)), "kernel_times")
+        raw = names.raw
+        out = {}
+        for i in range(min(n.value, cap)):
+            nm = raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode()
+            out[nm] = (float(ms[i]), int(cnt[i]))
+        return out
+
     @property
     def kernel_launches(self) -> int:
         return int(N.lib().tsdf_kernel_launches(self._h))

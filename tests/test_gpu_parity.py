@@ -159,9 +159,9 @@ def test_point_cloud_edge_cases_vs_oracle():
     rng = np.random.default_rng(3)
     for pts in [np.array([[0.51, 0.0, 0.0]]), np.zeros((0, 3)),
                 np.array([[0.5, 0, 0], [np.nan, 0, 0], [np.inf, 1, 1], [0, 0, 0]]),
-                rng.uniform(0.2, 0.7, size=(100, 3)), rng.normal(0, 8, (2000, 3))]:
-        g = PU.GpuBackend(8209, 0.08, (20000, 256))
-        o = PU.OracleBackend(8209, 0.08, (20000, 256))
+                rng.uniform(0.2, 0.7, size=(100, 3)), rng.normal(0, 1.5, (2000, 3))]:
+        g = PU.GpuBackend(1000003, 0.08, (400000, 256))
+        o = PU.OracleBackend(1000003, 0.08, (400000, 256))
         f = P.PointCloudFrame(points=pts, pose=P.SensorPose.identity())
         assert g.points(f, 0.04) == o.points(f, 0.04)
         assert g.points(f, 0.04) == o.points(f, 0.04)  # same frame twice
@@ -240,6 +240,24 @@ def test_table_ops_and_capacity_semantics():
         small.insert((2, 0, 0), 0)
 
 
+def test_capacity_error_parity_with_oracle():
+    """A scan that overflows the reference's bucket+chain limit raises
+    CapacityError on both sides (the reference raises on the 18th entry of a
+    Teschner slot, hashgrid.py:232-244)."""
+    import paper_2511_21459_b200 as P
+    from oracle.oracle import OracleError
+    pts = np.random.default_rng(3).normal(0, 8, (2000, 3))
+    f = P.PointCloudFrame(points=pts, pose=P.SensorPose.identity())
+    g = PU.GpuBackend(8209, 0.08, (400000, 256))
+    o = PU.OracleBackend(8209, 0.08, (400000, 256))
+    with pytest.raises(P.CapacityError):
+        g.points(f, 0.04)
+    with pytest.raises(OracleError) as e:
+        o.points(f, 0.04)
+    assert e.value.kind == "CapacityError"
+    assert g.t.live_count() == 0  # GPU rolls the whole frame back (DESIGN.md)
+
+
 def test_frame_capacity_error_rolls_back():
     import paper_2511_21459_b200 as P
     f = P.synth.render_frames("room", 1, 64, 48)[0]
@@ -253,7 +271,7 @@ def test_deterministic_rerun_bit_identical():
     digests = []
     for _ in range(2):
         b, _, _, _ = PU.run_depth_scenario("gpu", "sphere", 12, 48, 36, 0.08, 0.04,
-                                           (8192, 1024), 8209, sigma=2.5e-4, cadence=6)
+                                           (20000, 4096), 100003, sigma=2.5e-4, cadence=6)
         digests.append(PU.state_digest(b.state()))
         b.close()
     assert digests[0] == digests[1]
