@@ -1,20 +1,988 @@
-// mixed-resolution Marching Cubes (placeholder until the GPU extractor lands)
+// Mixed-resolution Marching Cubes over the device-resident grid
+// (reference meshing.py:94-552), bit-identical to the reference output.
+//
+// Stages (all on the device):
+//   M1  per live block: observed tsdf range (w > 0)                 k_block_range
+//   M2  27-neighbourhood range cull, per-level kept list            k_keep
+//   M3  canonical order: radix sort of packed keys per level; 256-block
+//       chunks as in the reference (meshing.py:457-459)
+//   M4  pass A, one CTA per kept block: corner gather (cross-level
+//       blend), gradients, cases -> cut-edge / triangle counts        k_mc<false>
+//   M5  exclusive scans of the counts laid out in the reference's emission
+//       order (level, chunk, axis, block) / (level, chunk, slot, block)
+//   M6  pass B: the same CTA recomputes and writes vertices + triangles  k_mc<true>
+//   M7  exact vertex dedup: stable LSD radix sort on (x, y, z) f64 keys,
+//       merged normals summed in emission order, winding fix, then the
+//       epsilon-bucket collapse (same sort on int64 cells) and compaction.
+#include <cub/cub.cuh>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
+
 #include "fusion.h"
+#include "mc_tables.h"
+
 namespace tsdf {
+
+#define MCK(x)                                  \
+  do {                                          \
+    int _s = cuda_status((x), #x);              \
+    if (_s) return _s;                          \
+  } while (0)
+
+__constant__ int8_t c_corner[8][3];
+__constant__ int8_t c_edge_loc[12][4];
+__constant__ uint16_t c_edge_table[256];
+__constant__ int8_t c_tri_table[256][16];
+
+static bool g_tables_loaded = false;
+static int load_tables() {
+  if (g_tables_loaded) return kOk;
+  MCK(cudaMemcpyToSymbol(c_corner, MC_CORNER, sizeof(MC_CORNER)));
+  MCK(cudaMemcpyToSymbol(c_edge_loc, MC_EDGE_LOC, sizeof(MC_EDGE_LOC)));
+  MCK(cudaMemcpyToSymbol(c_edge_table, MC_EDGE_TABLE, sizeof(MC_EDGE_TABLE)));
+  MCK(cudaMemcpyToSymbol(c_tri_table, MC_TRI_TABLE, sizeof(MC_TRI_TABLE)));
+  g_tables_loaded = true;
+  return kOk;
+}
+
+// scratch buffers owned by one extraction call
+struct DevBuf {
+  std::vector<void*> ptrs;
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// M1 / M2
+// ---------------------------------------------------------------------------
+
+// observed tsdf range of every live block (meshing.py:428-438); one warp per slot
+__global__ void k_block_range(DevTable t, uint8_t* obs, double* rlo, double* rhi) {
+  const int lane = threadIdx.x & 31;
+  uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t s = warp; s <= t.mask; s += nw) {
+    uint64_t k = t.keys[s];
+    uint32_t v = t.vals[s];
+    bool live = key_live(k) && v != kPending;
+    if (!live) {
+      if (lane == 0) obs[s] = 0;
+      continue;
+    }
+    const DevHeap& h = t.heap[val_level(v)];
+    int64_t base = (int64_t)val_handle(v) * h.nvox;
+    double lo = CUDART_INF_F, hi = -CUDART_INF_F;
+    bool any = false;
+    for (int i = lane; i < h.nvox; i += 32) {
+      if (h.weight[base + i] > 0.0f) {
+        double d = h.tsdf[base + i];
+        lo = fmin(lo, d);
+        hi = fmax(hi, d);
+        any = true;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) {
+      obs[s] = any;
+      rlo[s] = lo;
+      rhi[s] = hi;
+    }
+  }
+}
+
+// 27-neighbourhood straddle test (meshing.py:440-456); appends kept blocks
+// per level as (packed key, slot)
+__global__ void k_keep(DevTable t, const uint8_t* obs, const double* rlo, const double* rhi,
+                       double iso, uint64_t* keys_out, uint32_t* slots_out, uint64_t cap_per_level,
+                       unsigned long long* counts) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s <= t.mask;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    if (!obs[s]) continue;
+    uint64_t key = t.keys[s];
+    int64_t c[3];
+    unpack_key(key, c);
+    double lo = CUDART_INF, hi = -CUDART_INF;
+    for (int q = 0; q < 27; q++) {
+      int64_t n0 = c[0] + q / 9 - 1, n1 = c[1] + (q / 3) % 3 - 1, n2 = c[2] + q % 3 - 1;
+      if (!key_in_range(n0, n1, n2)) continue;
+      int64_t ns = table_find(t, pack_key(n0, n1, n2));
+      if (ns < 0 || !obs[ns]) continue;
+      lo = fmin(lo, rlo[ns]);
+      hi = fmax(hi, rhi[ns]);
+    }
+    if (lo <= iso && iso <= hi) {
+      int level = val_level(t.vals[s]);
+      unsigned long long i = atomicAdd(&counts[level], 1ull);
+      keys_out[level * cap_per_level + i] = key;
+      slots_out[level * cap_per_level + i] = (uint32_t)s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// M4 / M6: per-block Marching Cubes (meshing.py:94-158, 252-409)
+// ---------------------------------------------------------------------------
+
+constexpr int kMcThreads = 256;
+constexpr int kMaxN1 = 9;
+constexpr int kMaxCorners = kMaxN1 * kMaxN1 * kMaxN1;  // 729
+
+struct NbInfo {
+  int32_t found, level;
+  int64_t handle;
+};
+
+struct McSmem {
+  NbInfo nb[27];
+  double axes[3][kMaxN1];
+  double val[kMaxCorners];
+  double col[kMaxCorners][3];
+  double grad[kMaxCorners][3];
+  uint8_t valid[kMaxCorners];
+  uint8_t cases[512];
+  int16_t erank[3][kMaxN1 * kMaxN1 * (kMaxN1 - 1)];  // rank of each cut edge (pass B)
+};
+
+struct McArgs {
+  DevTable t;
+  const uint32_t* slots;     // kept blocks, canonical order, levels concatenated
+  const int32_t* blk_level;  // level of each kept block
+  const int64_t* chunk_of;   // global chunk id of each kept block
+  const int64_t* chunk_start;
+  const int32_t* chunk_size;
+  uint64_t n_blocks;
+  double iso;
+  // pass A outputs
+  int32_t* edge_cnt;  // [n_blocks][3]
+  int32_t* tri_cnt;   // [n_blocks][5]
+  uint8_t* emit_any;  // [n_blocks]
+  // pass B inputs / outputs
+  const uint8_t* chunk_emits;
+  const int64_t* voff;  // exclusive scan over (chunk, axis, block) sequence
+  const int64_t* toff;  // exclusive scan over (chunk, slot, block) sequence
+  double* vpos;         // raw vertices, half units, 3 per row
+  double* vnrm;
+  double* vcol;
+  int64_t* tri;  // raw vertex ids, 3 per row
+};
+
+__device__ inline double pw8(const double* a) {
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
+__device__ inline int64_t floordiv16(int64_t a) { return a >= 0 ? a / 16 : -((15 - a) / 16); }
+
+// corner blend of the up-to-8 octant voxels meeting lattice point h
+// (block-local half units) -- _gather, meshing.py:94-158
+__device__ void gather_corner(const DevTable& t, const NbInfo* nb, const int64_t* c,
+                              const int64_t* h, double* value, uint8_t* valid, double* color) {
+  double w[8], sdf[8], col[8][3];
+  int64_t key[8];
+#pragma unroll
+  for (int o = 0; o < 8; o++) {
+    const int so[3] = {(o >> 2 & 1) ? 1 : -1, (o >> 1 & 1) ? 1 : -1, (o & 1) ? 1 : -1};
+    int64_t off[3], local[3], v3[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      int64_t probe = h[a] + so[a];
+      off[a] = floordiv16(probe);
+      local[a] = probe - off[a] * 16;
+    }
+    const NbInfo& e = nb[((off[0] + 1) * 3 + (off[1] + 1)) * 3 + (off[2] + 1)];
+    int lvl = e.found ? e.level : 0;
+    int64_t csize = (int64_t)2 << lvl, side = 16 / csize;
+#pragma unroll
+    for (int a = 0; a < 3; a++) v3[a] = local[a] / csize;
+    double wob = 0.0;
+    sdf[o] = 0.0;
+    col[o][0] = col[o][1] = col[o][2] = 0.0;
+    if (e.found) {
+      uint64_t g0 = (uint64_t)((c[0] + off[0]) * side + v3[0] + (1 << 19));
+      uint64_t g1 = (uint64_t)((c[1] + off[1]) * side + v3[1] + (1 << 19));
+      uint64_t g2 = (uint64_t)((c[2] + off[2]) * side + v3[2] + (1 << 19));
+      key[o] = (int64_t)(((uint64_t)lvl << 60) | (g0 << 40) | (g1 << 20) | g2);
+      const DevHeap& hp = t.heap[lvl];
+      int64_t flat = e.handle * hp.nvox + (v3[0] * side + v3[1]) * side + v3[2];
+      size_t plane = (size_t)hp.cap * hp.nvox;
+      sdf[o] = hp.tsdf[flat];
+      wob = (double)hp.weight[flat];
+      col[o][0] = (double)hp.color[flat];
+      col[o][1] = (double)hp.color[plane + flat];
+      col[o][2] = (double)hp.color[2 * plane + flat];
+    } else {
+      key[o] = -1;
+    }
+    bool dup = false;
+    for (int i = 0; i < o; i++) dup |= key[o] == key[i];
+    dup &= (bool)e.found;
+    double m[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      double center = (double)(off[a] * 16) + ((double)v3[a] + 0.5) * (double)csize;
+      double x = 1.0 - fabs((double)h[a] - center) / (double)csize;
+      m[a] = x > 0.0 ? x : 0.0;
+    }
+    double coeff = (m[0] * m[1]) * m[2];
+    w[o] = (((coeff * (2.0 / (double)csize)) * (double)(wob > 0)) * (double)(e.found != 0)) *
+           (double)(!dup);
+  }
+  double wsum = pw8(w);
+  bool ok = wsum > 0;
+  double denom = ok ? wsum : 1.0;
+  double ws[8];
+#pragma unroll
+  for (int o = 0; o < 8; o++) ws[o] = w[o] * sdf[o];
+  *value = ok ? pw8(ws) / denom : 0.0;
+  *valid = ok;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    double acc = 0.0;
+#pragma unroll
+    for (int o = 0; o < 8; o++) acc += w[o] * col[o][k];
+    color[k] = acc / denom;
+  }
+}
+
+template <bool kWrite>
+__global__ void __launch_bounds__(kMcThreads) k_mc(McArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  McSmem& S = *reinterpret_cast<McSmem*>(smem_raw);
+  typedef cub::BlockScan<int32_t, kMcThreads> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int32_t s_total;
+  const int tid = threadIdx.x;
+  for (uint64_t gb = blockIdx.x; gb < A.n_blocks; gb += gridDim.x) {
+    if (kWrite && !A.chunk_emits[A.chunk_of[gb]]) continue;
+    const uint32_t slot = A.slots[gb];
+    const int level = A.blk_level[gb];
+    const int side = kFineSide >> level, n1 = side + 1, n3 = n1 * n1 * n1;
+    int64_t c[3];
+    unpack_key(A.t.keys[slot], c);
+    if (tid < 27) {
+      int64_t n0 = c[0] + tid / 9 - 1, nn1 = c[1] + (tid / 3) % 3 - 1, n2 = c[2] + tid % 3 - 1;
+      int64_t s = key_in_range(n0, nn1, n2) ? table_find(A.t, pack_key(n0, nn1, n2)) : -1;
+      uint32_t v = s >= 0 ? A.t.vals[s] : kPending;
+      bool f = s >= 0 && v != kPending;
+      S.nb[tid].found = f;
+      S.nb[tid].level = f ? val_level(v) : 0;
+      S.nb[tid].handle = f ? (int64_t)val_handle(v) : -1;
+    }
+    __syncthreads();
+    // corner planes with transition truncation (meshing.py:252-262, 312-321)
+    if (tid < 3 * n1) {
+      int a = tid / n1, i = tid % n1;
+      double step = (double)(16 / side);
+      double x = (double)i * step;
+      if (level > 0) {
+        const int lo_face[3] = {4, 10, 12}, hi_face[3] = {22, 16, 14};
+        const NbInfo& L = S.nb[lo_face[a]];
+        const NbInfo& H = S.nb[hi_face[a]];
+        if (i == 0 && L.found && L.level < level) x += step / 2;
+        if (i == side && H.found && H.level < level) x -= step / 2;
+      }
+      S.axes[a][i] = x;
+    }
+    __syncthreads();
+    for (int ci = tid; ci < n3; ci += kMcThreads) {
+      int i = ci / (n1 * n1), j = (ci / n1) % n1, k = ci % n1;
+      int64_t h[3] = {(int64_t)S.axes[0][i], (int64_t)S.axes[1][j], (int64_t)S.axes[2][k]};
+      gather_corner(A.t, S.nb, c, h, &S.val[ci], &S.valid[ci], S.col[ci]);
+    }
+    __syncthreads();
+    // central differences (meshing.py:265-297)
+    for (int ci = tid; ci < n3; ci += kMcThreads) {
+      int idx[3] = {ci / (n1 * n1), (ci / n1) % n1, ci % n1};
+      const int stride[3] = {n1 * n1, n1, 1};
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        int p = idx[a];
+        int lo = p == 0 ? 0 : p - 1, hi = p == n1 - 1 ? p : p + 1;
+        double num = S.val[ci + (hi - p) * stride[a]] - S.val[ci + (lo - p) * stride[a]];
+        S.grad[ci][a] = num / (S.axes[a][hi] - S.axes[a][lo]);
+      }
+    }
+    // cases
+    const int ncell = side * side * side;
+    int any = 0;
+    for (int cell = tid; cell < ncell; cell += kMcThreads) {
+      int i = cell / (side * side), j = (cell / side) % side, k = cell % side;
+      int cs = 0;
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        int ci = ((i + c_corner[q][0]) * n1 + (j + c_corner[q][1])) * n1 + (k + c_corner[q][2]);
+        cs |= (S.val[ci] < A.iso) << q;
+        ok &= S.valid[ci] != 0;
+      }
+      if (!ok) cs = 0;
+      S.cases[cell] = (uint8_t)cs;
+      any |= c_edge_table[cs] != 0;
+    }
+    any = __syncthreads_or(any);
+    if (!kWrite && tid == 0) A.emit_any[gb] = (uint8_t)any;
+    const int64_t G = A.chunk_of[gb];
+    const int64_t cstart = A.chunk_start[G];
+    const int32_t csize = A.chunk_size[G];
+    const int64_t bi = (int64_t)gb - cstart;
+    // cut edges per axis, C order over the axis-shaped grid
+    for (int a = 0; a < 3; a++) {
+      const int d0 = a == 0 ? side : n1, d1 = a == 1 ? side : n1, d2 = a == 2 ? side : n1;
+      const int ne = d0 * d1 * d2;
+      const int per = (ne + kMcThreads - 1) / kMcThreads;
+      int32_t mine = 0;
+      for (int e = tid * per; e < min(ne, (tid + 1) * per); e++) {
+        int i = e / (d1 * d2), j = (e / d2) % d1, k = e % d2;
+        int c0 = (i * n1 + j) * n1 + k;
+        int c1 = ((i + (a == 0)) * n1 + (j + (a == 1))) * n1 + (k + (a == 2));
+        mine += ((S.val[c0] < A.iso) != (S.val[c1] < A.iso)) && S.valid[c0] && S.valid[c1];
+      }
+      int32_t ex, tot;
+      Scan(scan_tmp).ExclusiveSum(mine, ex, tot);
+      __syncthreads();
+      if (!kWrite) {
+        if (tid == 0) A.edge_cnt[gb * 3 + a] = tot;
+      } else {
+        int64_t base = A.voff[3 * cstart + (int64_t)a * csize + bi] + ex;
+        const double wh[3] = {(double)c[0] * 16.0, (double)c[1] * 16.0, (double)c[2] * 16.0};
+        for (int e = tid * per; e < min(ne, (tid + 1) * per); e++) {
+          int i = e / (d1 * d2), j = (e / d2) % d1, k = e % d2;
+          int i1 = i + (a == 0), j1 = j + (a == 1), k1 = k + (a == 2);
+          int c0 = (i * n1 + j) * n1 + k, c1 = (i1 * n1 + j1) * n1 + k1;
+          bool cut = ((S.val[c0] < A.iso) != (S.val[c1] < A.iso)) && S.valid[c0] && S.valid[c1];
+          S.erank[a][e] = (int16_t)(base - A.voff[3 * cstart + (int64_t)a * csize + bi]);
+          if (!cut) continue;
+          double tt = (A.iso - S.val[c0]) / (S.val[c1] - S.val[c0]);
+          double p0[3] = {S.axes[0][i], S.axes[1][j], S.axes[2][k]};
+          double p1[3] = {S.axes[0][i1], S.axes[1][j1], S.axes[2][k1]};
+#pragma unroll
+          for (int d = 0; d < 3; d++) {
+            A.vpos[3 * base + d] = (p0[d] + tt * (p1[d] - p0[d])) + wh[d];
+            A.vnrm[3 * base + d] = S.grad[c0][d] + tt * (S.grad[c1][d] - S.grad[c0][d]);
+            A.vcol[3 * base + d] = S.col[c0][d] + tt * (S.col[c1][d] - S.col[c0][d]);
+          }
+          base++;
+        }
+      }
+    }
+    __syncthreads();
+    // triangles: slot-major, then cells in (i, j, k) order (meshing.py:385-409)
+    const int cper = (ncell + kMcThreads - 1) / kMcThreads;
+    for (int k3 = 0; k3 < 5; k3++) {
+      int32_t mine = 0;
+      for (int cell = tid * cper; cell < min(ncell, (tid + 1) * cper); cell++) {
+        int cs = S.cases[cell];
+        mine += c_edge_table[cs] != 0 && c_tri_table[cs][3 * k3] >= 0;
+      }
+      int32_t ex, tot;
+      Scan(scan_tmp).ExclusiveSum(mine, ex, tot);
+      __syncthreads();
+      if (!kWrite) {
+        if (tid == 0) A.tri_cnt[gb * 5 + k3] = tot;
+        continue;
+      }
+      int64_t base = A.toff[5 * cstart + (int64_t)k3 * csize + bi] + ex;
+      for (int cell = tid * cper; cell < min(ncell, (tid + 1) * cper); cell++) {
+        int cs = S.cases[cell];
+        if (!(c_edge_table[cs] != 0 && c_tri_table[cs][3 * k3] >= 0)) continue;
+        int ci = cell / (side * side), cj = (cell / side) % side, ck = cell % side;
+        for (int sidx = 0; sidx < 3; sidx++) {
+          int e = c_tri_table[cs][3 * k3 + sidx];
+          int a = c_edge_loc[e][0];
+          int ii = ci + c_edge_loc[e][1], jj = cj + c_edge_loc[e][2], kk = ck + c_edge_loc[e][3];
+          // rank of this cut edge among the block's axis-a cut edges
+          const int d1 = a == 1 ? side : n1, d2 = a == 2 ? side : n1;
+          int rank = S.erank[a][(ii * d1 + jj) * d2 + kk];
+          A.tri[3 * base + sidx] = A.voff[3 * cstart + (int64_t)a * csize + bi] + rank;
+        }
+        base++;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// M7: dedup, normals, winding, collapse
+// ---------------------------------------------------------------------------
+
+__device__ inline uint64_t f64_order_key(double x) {
+  x = x + 0.0;  // -0.0 -> +0.0 so equal values sort together
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_iota(uint64_t* v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = i;
+}
+
+// keys for one LSD pass: component d of the row each index points to
+__global__ void k_pos_keys(const double* pos, const uint64_t* idx, uint64_t n, int d, uint64_t* keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = f64_order_key(pos[3 * idx[i] + d]);
+}
+__global__ void k_cell_keys(const int64_t* cells, const uint64_t* idx, uint64_t n, int d,
+                            uint64_t* keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = (uint64_t)cells[3 * idx[i] + d] ^ 0x8000000000000000ull;
+}
+
+// group-start flags over a sorted index list; rows equal iff all 3 comps equal
+template <typename T>
+__global__ void k_group_flags(const T* rows, const uint64_t* idx, uint64_t n, int64_t* flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    bool start = i == 0;
+    if (!start) {
+      const T* a = rows + 3 * idx[i];
+      const T* b = rows + 3 * idx[i - 1];
+      start = !(a[0] == b[0] && a[1] == b[1] && a[2] == b[2]);
+    }
+    flag[i] = start;
+  }
+}
+
+// inclusive-scan ids -> inverse map and group starts
+__global__ void k_group_assign(const uint64_t* idx, const int64_t* gid_incl, uint64_t n,
+                               int64_t* inverse, int64_t* group_start) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t g = gid_incl[i] - 1;
+    inverse[idx[i]] = g;
+    if (i == 0 || gid_incl[i] != gid_incl[i - 1]) group_start[g] = (int64_t)i;
+  }
+}
+
+__device__ inline double norm_rows3(double x, double y, double z) {
+  return sqrt((x * x + y * y) + z * z);
+}
+
+// exact dedup outputs (meshing.py:468-479): first occurrence position/colour,
+// normals summed in emission order then normalised
+__global__ void k_dedup_out(const double* vpos, const double* vnrm, const double* vcol,
+                            const uint64_t* idx, const int64_t* gstart, int64_t ng, uint64_t n,
+                            double scale, double* v, double* nrm, double* col) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = gstart[g], e = g + 1 < ng ? gstart[g + 1] : (int64_t)n;
+    uint64_t first = idx[b];
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int64_t i = b; i < e; i++)
+      for (int k = 0; k < 3; k++) s[k] += vnrm[3 * idx[i] + k];
+    double nr = norm_rows3(s[0], s[1], s[2]);
+    for (int k = 0; k < 3; k++) {
+      v[3 * g + k] = vpos[3 * first + k] * scale;
+      double c = vcol[3 * first + k];
+      col[3 * g + k] = c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
+      nrm[3 * g + k] = nr > 0 ? s[k] / nr : (k == 2 ? 1.0 : 0.0);
+    }
+  }
+}
+
+// triangles through the dedup map, then winding fix (meshing.py:490-499)
+__global__ void k_orient(const int64_t* tri_raw, const int64_t* inverse, uint64_t nt,
+                         const double* v, const double* nrm, int64_t* tri) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t a = inverse[tri_raw[3 * i]], b = inverse[tri_raw[3 * i + 1]], c = inverse[tri_raw[3 * i + 2]];
+    double e1[3], e2[3], ref[3];
+    for (int k = 0; k < 3; k++) {
+      e1[k] = v[3 * b + k] - v[3 * a + k];
+      e2[k] = v[3 * c + k] - v[3 * a + k];
+      ref[k] = (nrm[3 * a + k] + nrm[3 * b + k]) + nrm[3 * c + k];
+    }
+    double g0 = e1[1] * e2[2] - e1[2] * e2[1];
+    double g1 = e1[2] * e2[0] - e1[0] * e2[2];
+    double g2 = e1[0] * e2[1] - e1[1] * e2[0];
+    bool flip = ((g0 * ref[0] + g2 * ref[2]) + g1 * ref[1]) < 0;
+    tri[3 * i] = flip ? c : a;
+    tri[3 * i + 1] = b;
+    tri[3 * i + 2] = flip ? a : c;
+  }
+}
+
+__global__ void k_cells(const double* v, uint64_t n, double eps, int64_t* cells) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 3 * n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    cells[i] = (int64_t)floor(v[i] / eps);
+}
+
+// collapse_vertices (meshing.py:502-545): centroid / normalised-normal / mean colour
+// per bucket, members summed in vertex order; eps == 0 keeps first occurrences
+__global__ void k_collapse_out(const double* v, const double* nrm, const double* col,
+                               const uint64_t* idx, const int64_t* gstart, int64_t ng, uint64_t n,
+                               int exact, double* ov, double* on, double* oc) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = gstart[g], e = g + 1 < ng ? gstart[g + 1] : (int64_t)n;
+    if (exact) {
+      uint64_t f = idx[b];
+      for (int k = 0; k < 3; k++) {
+        ov[3 * g + k] = v[3 * f + k];
+        on[3 * g + k] = nrm[3 * f + k];
+        oc[3 * g + k] = col[3 * f + k];
+      }
+      continue;
+    }
+    double sv[3] = {0, 0, 0}, sn[3] = {0, 0, 0}, sc[3] = {0, 0, 0};
+    for (int64_t i = b; i < e; i++) {
+      uint64_t r = idx[i];
+      for (int k = 0; k < 3; k++) {
+        sv[k] += v[3 * r + k];
+        sn[k] += nrm[3 * r + k];
+        sc[k] += col[3 * r + k];
+      }
+    }
+    double cnt = (double)(e - b);
+    double nr = norm_rows3(sn[0], sn[1], sn[2]);
+    double d = nr > 0 ? nr : 1.0;
+    for (int k = 0; k < 3; k++) {
+      ov[3 * g + k] = sv[k] / cnt;
+      on[3 * g + k] = sn[k] / d;
+      oc[3 * g + k] = sc[k] / cnt;
+    }
+  }
+}
+
+// remap triangles, drop repeated-index and sub-1e-12 m^2 ones, mark used vertices
+__global__ void k_tri_filter(const int64_t* tri, const int64_t* inverse, uint64_t nt,
+                             const double* v, int64_t* tri_out, int64_t* keep, uint8_t* used) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t a = inverse[tri[3 * i]], b = inverse[tri[3 * i + 1]], c = inverse[tri[3 * i + 2]];
+    bool ok = a != b && b != c && a != c;
+    if (ok) {
+      double e1[3], e2[3];
+      for (int k = 0; k < 3; k++) {
+        e1[k] = v[3 * b + k] - v[3 * a + k];
+        e2[k] = v[3 * c + k] - v[3 * a + k];
+      }
+      double x = e1[1] * e2[2] - e1[2] * e2[1];
+      double y = e1[2] * e2[0] - e1[0] * e2[2];
+      double z = e1[0] * e2[1] - e1[1] * e2[0];
+      ok = 0.5 * norm_rows3(x, y, z) >= 1e-12;
+    }
+    keep[i] = ok;
+    tri_out[3 * i] = a;
+    tri_out[3 * i + 1] = b;
+    tri_out[3 * i + 2] = c;
+    if (ok) used[a] = used[b] = used[c] = 1;
+  }
+}
+
+__global__ void k_u8_to_i64(const uint8_t* a, uint64_t n, int all, int64_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = all ? 1 : a[i];
+}
+
+__global__ void k_compact_verts(const double* v, const double* n, const double* c,
+                                const int64_t* used, const int64_t* remap, uint64_t nv, double* ov,
+                                double* on, double* oc) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!used[i]) continue;
+    int64_t r = remap[i];
+    for (int k = 0; k < 3; k++) {
+      ov[3 * r + k] = v[3 * i + k];
+      on[3 * r + k] = n[3 * i + k];
+      oc[3 * r + k] = c[3 * i + k];
+    }
+  }
+}
+
+__global__ void k_compact_tris(const int64_t* tri, const int64_t* keep, const int64_t* pos,
+                               const int64_t* remap, uint64_t nt, int64_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    int64_t p = pos[i];
+    for (int k = 0; k < 3; k++) out[3 * p + k] = remap[tri[3 * i + k]];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
+static unsigned gridn(uint64_t n) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 32));
+}
+
+struct Scratch {
+  DevBuf bufs;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  ~Scratch() {
+    if (tmp) cudaFree(tmp);
+  }
+  int need(size_t b) {
+    if (b <= tmp_bytes) return kOk;
+    if (tmp) cudaFree(tmp);
+    tmp = nullptr;
+    tmp_bytes = 0;
+    if (cudaMalloc(&tmp, b) != cudaSuccess) {
+      set_error("device allocation failed for sort scratch");
+      return kCapacityError;
+    }
+    tmp_bytes = b;
+    return kOk;
+  }
+};
+
+static int exclusive_scan(Scratch& S, const int64_t* in, int64_t* out, uint64_t n, cudaStream_t st) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, in, out, (int64_t)n, st);
+  if (int s = S.need(b)) return s;
+  MCK(cub::DeviceScan::ExclusiveSum(S.tmp, b, in, out, (int64_t)n, st));
+  return kOk;
+}
+static int inclusive_scan(Scratch& S, const int64_t* in, int64_t* out, uint64_t n, cudaStream_t st) {
+  size_t b = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, b, in, out, (int64_t)n, st);
+  if (int s = S.need(b)) return s;
+  MCK(cub::DeviceScan::InclusiveSum(S.tmp, b, in, out, (int64_t)n, st));
+  return kOk;
+}
+
+// stable lexicographic order of 3-component rows: LSD radix passes z, y, x
+template <typename T, bool kFloat>
+static int sort_rows(Scratch& S, const T* rows, uint64_t n, uint64_t* idx, cudaStream_t st) {
+  uint64_t* keys = S.bufs.get<uint64_t>(n);
+  uint64_t* keys2 = S.bufs.get<uint64_t>(n);
+  uint64_t* idx2 = S.bufs.get<uint64_t>(n);
+  if (!keys || !keys2 || !idx2) return kCapacityError;
+  k_iota<<<gridn(n), 256, 0, st>>>(idx, n);
+  for (int d = 2; d >= 0; d--) {
+    if (kFloat)
+      k_pos_keys<<<gridn(n), 256, 0, st>>>((const double*)rows, idx, n, d, keys);
+    else
+      k_cell_keys<<<gridn(n), 256, 0, st>>>((const int64_t*)rows, idx, n, d, keys);
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, keys, keys2, idx, idx2, (int64_t)n, 0, 64, st);
+    if (int s = S.need(b)) return s;
+    MCK(cub::DeviceRadixSort::SortPairs(S.tmp, b, keys, keys2, idx, idx2, (int64_t)n, 0, 64, st));
+    MCK(cudaMemcpyAsync(idx, idx2, n * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return kOk;
+}
+
+// unique over rows: inverse[n], group starts (in sorted order); returns ng
+template <typename T, bool kFloat>
+static int unique_rows(Scratch& S, const T* rows, uint64_t n, uint64_t* idx, int64_t* inverse,
+                       int64_t* gstart, int64_t* ng, cudaStream_t st) {
+  if (int s = sort_rows<T, kFloat>(S, rows, n, idx, st)) return s;
+  int64_t* flag = S.bufs.get<int64_t>(n);
+  int64_t* gid = S.bufs.get<int64_t>(n);
+  if (!flag || !gid) return kCapacityError;
+  k_group_flags<T><<<gridn(n), 256, 0, st>>>(rows, idx, n, flag);
+  if (int s = inclusive_scan(S, flag, gid, n, st)) return s;
+  k_group_assign<<<gridn(n), 256, 0, st>>>(idx, gid, n, inverse, gstart);
+  MCK(cudaMemcpyAsync(ng, gid + n - 1, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  return kOk;
+}
+
+// collapse + compaction on device arrays (consumes v/n/c/tri); fills host out
+static int collapse_device(Scratch& S, const double* v, const double* nrm, const double* col,
+                           uint64_t nv, const int64_t* tri, uint64_t nt, double eps,
+                           cudaStream_t st, MeshOut* out) {
+  memset(out, 0, sizeof(*out));
+  if (nv == 0) return kOk;
+  uint64_t* idx = S.bufs.get<uint64_t>(nv);
+  int64_t* inv = S.bufs.get<int64_t>(nv);
+  int64_t* gst = S.bufs.get<int64_t>(nv);
+  if (!idx || !inv || !gst) return kCapacityError;
+  int64_t ng = 0;
+  bool exact = eps == 0.0;
+  if (exact) {
+    if (int s = unique_rows<double, true>(S, v, nv, idx, inv, gst, &ng, st)) return s;
+  } else {
+    int64_t* cells = S.bufs.get<int64_t>(3 * nv);
+    if (!cells) return kCapacityError;
+    k_cells<<<gridn(3 * nv), 256, 0, st>>>(v, nv, eps, cells);
+    if (int s = unique_rows<int64_t, false>(S, cells, nv, idx, inv, gst, &ng, st)) return s;
+  }
+  double* cv = S.bufs.get<double>(3 * ng);
+  double* cn = S.bufs.get<double>(3 * ng);
+  double* cc = S.bufs.get<double>(3 * ng);
+  int64_t* tri2 = S.bufs.get<int64_t>(3 * nt);
+  int64_t* keep = S.bufs.get<int64_t>(nt);
+  int64_t* kpos = S.bufs.get<int64_t>(nt);
+  uint8_t* used8 = S.bufs.get<uint8_t>(ng);
+  int64_t* used = S.bufs.get<int64_t>(ng);
+  int64_t* remap = S.bufs.get<int64_t>(ng);
+  if (!cv || !cn || !cc || !tri2 || !keep || !kpos || !used8 || !used || !remap) return kCapacityError;
+  k_collapse_out<<<gridn(ng), 256, 0, st>>>(v, nrm, col, idx, gst, ng, nv, exact, cv, cn, cc);
+  MCK(cudaMemsetAsync(used8, 0, ng, st));
+  if (nt) k_tri_filter<<<gridn(nt), 256, 0, st>>>(tri, inv, nt, cv, tri2, keep, used8);
+  k_u8_to_i64<<<gridn(ng), 256, 0, st>>>(used8, ng, nt == 0, used);
+  if (int s = exclusive_scan(S, used, remap, ng, st)) return s;
+  int64_t last_r, last_u, last_p = 0, last_k = 0;
+  MCK(cudaMemcpyAsync(&last_r, remap + ng - 1, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(&last_u, used + ng - 1, 8, cudaMemcpyDeviceToHost, st));
+  if (nt) {
+    if (int s = exclusive_scan(S, keep, kpos, nt, st)) return s;
+    MCK(cudaMemcpyAsync(&last_p, kpos + nt - 1, 8, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(&last_k, keep + nt - 1, 8, cudaMemcpyDeviceToHost, st));
+  }
+  MCK(cudaStreamSynchronize(st));
+  int64_t nu = last_r + last_u, ntk = last_p + last_k;
+  double* fv = S.bufs.get<double>(3 * nu);
+  double* fn = S.bufs.get<double>(3 * nu);
+  double* fc = S.bufs.get<double>(3 * nu);
+  int64_t* ft = S.bufs.get<int64_t>(3 * ntk);
+  if (!fv || !fn || !fc || !ft) return kCapacityError;
+  k_compact_verts<<<gridn(ng), 256, 0, st>>>(cv, cn, cc, used, remap, ng, fv, fn, fc);
+  if (nt) k_compact_tris<<<gridn(nt), 256, 0, st>>>(tri2, keep, kpos, remap, nt, ft);
+  MCK(cudaGetLastError());
+  out->nv = nu;
+  out->nt = ntk;
+  out->v = (double*)malloc(std::max<int64_t>(nu, 1) * 24);
+  out->n = (double*)malloc(std::max<int64_t>(nu, 1) * 24);
+  out->c = (double*)malloc(std::max<int64_t>(nu, 1) * 24);
+  out->tri = (int64_t*)malloc(std::max<int64_t>(ntk, 1) * 24);
+  MCK(cudaMemcpyAsync(out->v, fv, nu * 24, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(out->n, fn, nu * 24, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(out->c, fc, nu * 24, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(out->tri, ft, ntk * 24, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  return kOk;
+}
+
 int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
-  (void)T; (void)iso; (void)eps; (void)out;
-  set_error("extract_mesh: not built yet");
-  return kValueError;
+  memset(out, 0, sizeof(*out));
+  if (eps < 0) {
+    set_error("epsilon must be non-negative");
+    return kValueError;
+  }
+  if (int s = load_tables()) return s;
+  cudaStream_t st = T->stream;
+  MCK(cudaStreamSynchronize(st));
+  const DevTable& d = T->d;
+  uint64_t slots = T->slots;
+  Scratch S;
+  uint8_t* obs = S.bufs.get<uint8_t>(slots);
+  double* rlo = S.bufs.get<double>(slots);
+  double* rhi = S.bufs.get<double>(slots);
+  int64_t live[kMaxLevels] = {0, 0, 0, 0}, total = 0;
+  for (int l = 0; l < d.n_levels; l++) {
+    if (int s = live_count(T, l, &live[l])) return s;
+    total = std::max<int64_t>(total, live[l]);
+  }
+  uint64_t cap = std::max<int64_t>(total, 1);
+  uint64_t* kkeys = S.bufs.get<uint64_t>(cap * kMaxLevels);
+  uint32_t* kslots = S.bufs.get<uint32_t>(cap * kMaxLevels);
+  unsigned long long* kcnt = S.bufs.get<unsigned long long>(kMaxLevels);
+  if (!obs || !rlo || !rhi || !kkeys || !kslots || !kcnt) {
+    set_error("device allocation failed for mesh scratch");
+    return kCapacityError;
+  }
+  MCK(cudaMemsetAsync(kcnt, 0, kMaxLevels * 8, st));
+  {
+    int _pid = prof_begin(T, "k_block_range");
+    k_block_range<<<148 * 16, 256, 0, st>>>(d, obs, rlo, rhi);
+    prof_end(T, _pid);
+  }
+  {
+    int _pid = prof_begin(T, "k_keep");
+    k_keep<<<gridn(slots), 256, 0, st>>>(d, obs, rlo, rhi, iso, kkeys, kslots, cap, kcnt);
+    prof_end(T, _pid);
+  }
+  T->launches += 2;
+  unsigned long long hcnt[kMaxLevels];
+  MCK(cudaMemcpyAsync(hcnt, kcnt, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  // canonical order per level, concatenated; chunks of 256 within a level
+  uint64_t nb = 0;
+  for (int l = 0; l < d.n_levels; l++) nb += hcnt[l];
+  if (nb == 0) return kOk;
+  uint64_t* skeys = S.bufs.get<uint64_t>(nb);
+  uint32_t* sslots = S.bufs.get<uint32_t>(nb);
+  int32_t* blevel = S.bufs.get<int32_t>(nb);
+  if (!skeys || !sslots || !blevel) return kCapacityError;
+  std::vector<int64_t> h_chunk_of(nb), h_chunk_start;
+  std::vector<int32_t> h_chunk_size, h_blevel(nb);
+  uint64_t off = 0;
+  for (int l = 0; l < d.n_levels; l++) {
+    uint64_t n = hcnt[l];
+    if (!n) continue;
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, kkeys + l * cap, skeys + off, kslots + l * cap,
+                                    sslots + off, (int64_t)n, 0, 63, st);
+    if (int s = S.need(b)) return s;
+    MCK(cub::DeviceRadixSort::SortPairs(S.tmp, b, kkeys + l * cap, skeys + off, kslots + l * cap,
+                                        sslots + off, (int64_t)n, 0, 63, st));
+    int64_t chunk_base = (int64_t)h_chunk_start.size();
+    for (uint64_t i = 0; i < n; i += 256) {
+      h_chunk_start.push_back((int64_t)(off + i));
+      h_chunk_size.push_back((int32_t)std::min<uint64_t>(256, n - i));
+    }
+    for (uint64_t i = 0; i < n; i++) {
+      h_chunk_of[off + i] = chunk_base + (int64_t)(i / 256);
+      h_blevel[off + i] = l;
+    }
+    off += n;
+  }
+  uint64_t nchunks = h_chunk_start.size();
+  int64_t* chunk_of = S.bufs.get<int64_t>(nb);
+  int64_t* chunk_start = S.bufs.get<int64_t>(nchunks);
+  int32_t* chunk_size = S.bufs.get<int32_t>(nchunks);
+  int32_t* edge_cnt = S.bufs.get<int32_t>(nb * 3);
+  int32_t* tri_cnt = S.bufs.get<int32_t>(nb * 5);
+  uint8_t* emit_any = S.bufs.get<uint8_t>(nb);
+  if (!chunk_of || !chunk_start || !chunk_size || !edge_cnt || !tri_cnt || !emit_any)
+    return kCapacityError;
+  MCK(cudaMemcpyAsync(chunk_of, h_chunk_of.data(), nb * 8, cudaMemcpyHostToDevice, st));
+  MCK(cudaMemcpyAsync(chunk_start, h_chunk_start.data(), nchunks * 8, cudaMemcpyHostToDevice, st));
+  MCK(cudaMemcpyAsync(chunk_size, h_chunk_size.data(), nchunks * 4, cudaMemcpyHostToDevice, st));
+  MCK(cudaMemcpyAsync(blevel, h_blevel.data(), nb * 4, cudaMemcpyHostToDevice, st));
+  McArgs A{};
+  A.t = d;
+  A.slots = sslots;
+  A.blk_level = blevel;
+  A.chunk_of = chunk_of;
+  A.chunk_start = chunk_start;
+  A.chunk_size = chunk_size;
+  A.n_blocks = nb;
+  A.iso = iso;
+  A.edge_cnt = edge_cnt;
+  A.tri_cnt = tri_cnt;
+  A.emit_any = emit_any;
+  size_t smem = sizeof(McSmem);
+  MCK(cudaFuncSetAttribute(k_mc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MCK(cudaFuncSetAttribute(k_mc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  unsigned g = (unsigned)std::min<uint64_t>(nb, 148 * 4);
+  {
+    int _pid = prof_begin(T, "k_mc_count");
+    k_mc<false><<<g, kMcThreads, smem, st>>>(A);
+    prof_end(T, _pid);
+  }
+  T->launches++;
+  MCK(cudaGetLastError());
+  // emission-order count sequences (host: small per-block arrays)
+  std::vector<int32_t> he(nb * 3), ht(nb * 5);
+  std::vector<uint8_t> hany(nb);
+  MCK(cudaMemcpyAsync(he.data(), edge_cnt, nb * 12, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(ht.data(), tri_cnt, nb * 20, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(hany.data(), emit_any, nb, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  std::vector<uint8_t> hce(nchunks, 0);
+  for (uint64_t b = 0; b < nb; b++) hce[h_chunk_of[b]] |= hany[b];
+  std::vector<int64_t> hvoff(nb * 3), htoff(nb * 5);
+  int64_t vtot = 0, ttot = 0;
+  for (uint64_t G = 0; G < nchunks; G++) {
+    int64_t cs = h_chunk_start[G], sz = h_chunk_size[G];
+    for (int a = 0; a < 3; a++)
+      for (int64_t b = 0; b < sz; b++) {
+        hvoff[3 * cs + a * sz + b] = vtot;
+        if (hce[G]) vtot += he[(cs + b) * 3 + a];
+      }
+    for (int k3 = 0; k3 < 5; k3++)
+      for (int64_t b = 0; b < sz; b++) {
+        htoff[5 * cs + k3 * sz + b] = ttot;
+        if (hce[G]) ttot += ht[(cs + b) * 5 + k3];
+      }
+  }
+  if (ttot == 0) return kOk;  // reference: no triangles -> empty mesh
+  uint8_t* chunk_emits = S.bufs.get<uint8_t>(nchunks);
+  int64_t* voff = S.bufs.get<int64_t>(nb * 3);
+  int64_t* toff = S.bufs.get<int64_t>(nb * 5);
+  double* vpos = S.bufs.get<double>(3 * vtot);
+  double* vnrm = S.bufs.get<double>(3 * vtot);
+  double* vcol = S.bufs.get<double>(3 * vtot);
+  int64_t* tri = S.bufs.get<int64_t>(3 * ttot);
+  if (!chunk_emits || !voff || !toff || !vpos || !vnrm || !vcol || !tri) {
+    set_error("device allocation failed for mesh output");
+    return kCapacityError;
+  }
+  MCK(cudaMemcpyAsync(chunk_emits, hce.data(), nchunks, cudaMemcpyHostToDevice, st));
+  MCK(cudaMemcpyAsync(voff, hvoff.data(), nb * 24, cudaMemcpyHostToDevice, st));
+  MCK(cudaMemcpyAsync(toff, htoff.data(), nb * 40, cudaMemcpyHostToDevice, st));
+  A.chunk_emits = chunk_emits;
+  A.voff = voff;
+  A.toff = toff;
+  A.vpos = vpos;
+  A.vnrm = vnrm;
+  A.vcol = vcol;
+  A.tri = tri;
+  {
+    int _pid = prof_begin(T, "k_mc_emit");
+    k_mc<true><<<g, kMcThreads, smem, st>>>(A);
+    prof_end(T, _pid);
+  }
+  T->launches++;
+  MCK(cudaGetLastError());
+  // exact dedup of bit-identical boundary vertices
+  uint64_t nv = (uint64_t)vtot, nt = (uint64_t)ttot;
+  uint64_t* idx = S.bufs.get<uint64_t>(nv);
+  int64_t* inv = S.bufs.get<int64_t>(nv);
+  int64_t* gst = S.bufs.get<int64_t>(nv);
+  if (!idx || !inv || !gst) return kCapacityError;
+  int64_t ng = 0;
+  if (int s = unique_rows<double, true>(S, vpos, nv, idx, inv, gst, &ng, st)) return s;
+  double* mv = S.bufs.get<double>(3 * ng);
+  double* mn = S.bufs.get<double>(3 * ng);
+  double* mc = S.bufs.get<double>(3 * ng);
+  int64_t* mt = S.bufs.get<int64_t>(3 * nt);
+  if (!mv || !mn || !mc || !mt) return kCapacityError;
+  double scale = d.edge / 16.0;
+  k_dedup_out<<<gridn(ng), 256, 0, st>>>(vpos, vnrm, vcol, idx, gst, ng, nv, scale, mv, mn, mc);
+  k_orient<<<gridn(nt), 256, 0, st>>>(tri, inv, nt, mv, mn, mt);
+  T->launches += 12;
+  MCK(cudaGetLastError());
+  int s = collapse_device(S, mv, mn, mc, (uint64_t)ng, mt, nt, eps, st, out);
+  prof_collect(T);
+  return s;
 }
+
+int collapse_vertices(const double* v, const double* n, const double* c, int64_t nv,
+                      const int64_t* tri, int64_t nt, double eps, MeshOut* out) {
+  memset(out, 0, sizeof(*out));
+  if (eps < 0) {
+    set_error("epsilon must be non-negative");
+    return kValueError;
+  }
+  if (nv == 0) return kOk;
+  Scratch S;
+  double* dv = S.bufs.get<double>(3 * nv);
+  double* dn = S.bufs.get<double>(3 * nv);
+  double* dc = S.bufs.get<double>(3 * nv);
+  int64_t* dt = S.bufs.get<int64_t>(3 * std::max<int64_t>(nt, 1));
+  if (!dv || !dn || !dc || !dt) return kCapacityError;
+  MCK(cudaMemcpy(dv, v, nv * 24, cudaMemcpyHostToDevice));
+  MCK(cudaMemcpy(dn, n, nv * 24, cudaMemcpyHostToDevice));
+  MCK(cudaMemcpy(dc, c, nv * 24, cudaMemcpyHostToDevice));
+  if (nt) MCK(cudaMemcpy(dt, tri, nt * 24, cudaMemcpyHostToDevice));
+  return collapse_device(S, dv, dn, dc, (uint64_t)nv, dt, (uint64_t)nt, eps, 0, out);
+}
+
 void mesh_free(MeshOut* m) {
-  free(m->v); free(m->n); free(m->c); free(m->tri);
+  free(m->v);
+  free(m->n);
+  free(m->c);
+  free(m->tri);
+  memset(m, 0, sizeof(*m));
 }
-}  // namespace tsdf
-namespace tsdf {
-int collapse_vertices(const double*, const double*, const double*, int64_t, const int64_t*,
-                      int64_t, double, MeshOut*) {
-  set_error("collapse_vertices: not built yet");
-  return kValueError;
-}
+
 }  // namespace tsdf
