@@ -303,3 +303,43 @@ def test_select_merge_candidates_matches_apply():
     st = P.apply_merges(b.t, 2.5e-4)
     assert st.merged == len(cands) > 0
     assert all(b.t.find(c)[1] == 1 for c in cands)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_block_key_sharding_union_equals_single_gpu(world):
+    """Multi-GPU path on one device: `world` shard tables (owner(key) == rank)
+    integrate the same frames + merges; the union of shards is the single
+    table bit-for-bit and the partitioned counters sum to its counters."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200.sharding import INVARIANT, PARTITIONED, owner_of_coords
+    frames = P.synth.render_frames("room", 20, 160, 120, depth_dtype=np.float32,
+                                   color_dtype=np.uint8)
+    full = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000))
+    shards = []
+    for r in range(world):
+        t = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000))
+        t.set_shard(r, world)
+        shards.append(t)
+    for i, f in enumerate(frames):
+        s_full = P.integrate_depth(full, f, 0.015)
+        parts = [P.integrate_depth(t, f, 0.015) for t in shards]
+        for k in PARTITIONED:
+            assert sum(getattr(p, k) for p in parts) == getattr(s_full, k), k
+        for k in INVARIANT:
+            assert all(getattr(p, k) == getattr(s_full, k) for p in parts), k
+        if (i + 1) % 10 == 0:
+            m = P.apply_merges(full, 2.5e-5).merged
+            assert sum(P.apply_merges(t, 2.5e-5).merged for t in shards) == m
+    for level in range(2):
+        co, _, ts, w, s2, col = full.export_level(level)
+        rows = {}
+        for r, t in enumerate(shards):
+            c2, _, t2, w2, s22, col2 = t.export_level(level)
+            assert np.all(owner_of_coords(c2, world) == r)
+            for j, c in enumerate(map(tuple, c2.tolist())):
+                rows[c] = (t2[j], w2[j], s22[j], col2[j])
+        assert set(rows) == set(map(tuple, co.tolist()))
+        for j, c in enumerate(map(tuple, co.tolist())):
+            a = rows[c]
+            assert np.array_equal(a[0], ts[j]) and np.array_equal(a[1], w[j])
+            assert np.array_equal(a[2], s2[j]) and np.array_equal(a[3], col[j])
