@@ -149,6 +149,16 @@ def integrate(P, t, wl, fr, device=None):
     return P.integrate_pointcloud(t, f, wl["tau"])
 
 
+def window(P, t, wl, frs, dev=None):
+    """One merge window through the public API: depth frames go through
+    integrate_depth_batch (one host sync per window), scans per scan."""
+    if wl["kind"] == "depth":
+        fs = [P.DepthFrame(depth=fr[0] if dev is None else dev[i][0], intrinsics=fr[3], pose=fr[2],
+                           color=fr[1] if dev is None else dev[i][1]) for i, fr in enumerate(frs)]
+        return P.integrate_depth_batch(t, fs, wl["tau"])
+    return [integrate(P, t, wl, fr, None if dev is None else dev[i]) for i, fr in enumerate(frs)]
+
+
 def kernel_bytes(stats_list, wl):
     """Algorithmic bytes: B = s_in*P + 16*T + 16*A + 48*U per frame."""
     s_in = S_IN[wl["kind"]]
@@ -194,9 +204,8 @@ def run_b200(args, wl, rank, world, dist, torch):
     all_stats, step_ms, merged = [], [], 0
     fi = 0
     for s in range(W):
-        for _ in range(FRAMES_PER_STEP):
-            integrate(P, table, wl, frames[fi], dframes[fi])
-            fi += 1
+        window(P, table, wl, frames[fi:fi + FRAMES_PER_STEP], dframes[fi:fi + FRAMES_PER_STEP])
+        fi += FRAMES_PER_STEP
         P.apply_merges(table, wl["sigma"], all_levels=True)
     table.profile(True)
     table.kernel_times(reset=True)
@@ -210,9 +219,9 @@ def run_b200(args, wl, rank, world, dist, torch):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for _ in range(FRAMES_PER_STEP):
-                all_stats.append(integrate(P, table, wl, frames[fi], dframes[fi]))
-                fi += 1
+            all_stats += window(P, table, wl, frames[fi:fi + FRAMES_PER_STEP],
+                                dframes[fi:fi + FRAMES_PER_STEP])
+            fi += FRAMES_PER_STEP
             merged += P.apply_merges(table, wl["sigma"], all_levels=True).merged
             e1.record(stream)
             e1.synchronize()
@@ -245,23 +254,22 @@ def run_b200(args, wl, rank, world, dist, torch):
     h2d = d2h = 0
     fi = 0
     for s in range(W):
-        for _ in range(FRAMES_PER_STEP):
-            integrate(P, t2, wl, pinned[fi])
-            fi += 1
+        window(P, t2, wl, pinned[fi:fi + FRAMES_PER_STEP])
+        fi += FRAMES_PER_STEP
         P.apply_merges(t2, wl["sigma"], all_levels=True)
     barrier()
     e2e_t0 = time.perf_counter()
     e2e_pts = 0
     for s in range(K):
-        for _ in range(FRAMES_PER_STEP):
-            fr = pinned[fi]
-            st = integrate(P, t2, wl, fr)
-            e2e_pts += st.measurements
+        win = pinned[fi:fi + FRAMES_PER_STEP]
+        sts = window(P, t2, wl, win)
+        e2e_pts += sum(st.measurements for st in sts)
+        for fr in win:
             h2d += fr[0].nbytes + (0 if fr[1] is None else fr[1].nbytes)
-            d2h += 256  # per-call counters block (stats) read back
-            fi += 1
+            d2h += 192  # per-frame counters block (stats) read back
+        fi += FRAMES_PER_STEP
         P.apply_merges(t2, wl["sigma"], all_levels=True)
-        d2h += 256
+        d2h += 192
     barrier()
     e2e_s = time.perf_counter() - e2e_t0
     if world > 1:

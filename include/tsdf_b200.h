@@ -96,6 +96,18 @@ int tsdf_integrate_depth(tsdf_table *t, const void *depth, int32_t depth_dtype, 
                          const double *K, const double *R, const double *trans, double tau,
                          double weight_cap, tsdf_integration_stats *stats);
 
+/* n_frames depth frames of one merge window (same size/dtypes), enqueued
+ * back to back with one host synchronisation.  Per-frame K (4), R (9) and
+ * trans (3) are packed consecutively.  Semantically identical to calling
+ * tsdf_integrate_depth per frame: on an error at frame i the frames after
+ * it leave the table untouched, *n_done = i and the error is returned. */
+int tsdf_integrate_depth_batch(tsdf_table *t, int32_t n_frames, const void *const *depth,
+                               int32_t depth_dtype, const void *const *rgb, int32_t rgb_dtype,
+                               int32_t height, int32_t width, int32_t mem, const double *K,
+                               const double *R, const double *trans, double tau,
+                               double weight_cap, tsdf_integration_stats *stats,
+                               int32_t *n_done);
+
 /* integrate_pointcloud(table, PointCloudFrame, tau, weight_cap) --
  * integrate.py:175-252.  xyz: n*3 sensor-frame points; rgb n*3 or NULL. */
 int tsdf_integrate_points(tsdf_table *t, const void *xyz, int32_t xyz_dtype, const void *rgb,

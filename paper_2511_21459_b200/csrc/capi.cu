@@ -1,5 +1,6 @@
 // extern "C" boundary (include/tsdf_b200.h) over the device implementation.
 #include <cstring>
+#include <vector>
 
 #include "../../include/tsdf_b200.h"
 #include "fusion.h"
@@ -269,6 +270,42 @@ int tsdf_profile_read(tsdf_table* t, int32_t reset, int32_t max_entries, char* n
   *n_out = i;
   if (reset) T->prof_acc.clear();
   return TSDF_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int tsdf_integrate_depth_batch(tsdf_table* t, int32_t n_frames, const void* const* depth,
+                               int32_t depth_dtype, const void* const* rgb, int32_t rgb_dtype,
+                               int32_t height, int32_t width, int32_t mem, const double* K,
+                               const double* R, const double* trans, double tau,
+                               double weight_cap, tsdf_integration_stats* stats,
+                               int32_t* n_done) {
+  NEED(t);
+  if (n_frames <= 0) {
+    *n_done = 0;
+    return TSDF_OK;
+  }
+  if (depth_dtype < 0 || depth_dtype > 3 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  std::vector<DepthArgs> args(n_frames);
+  for (int i = 0; i < n_frames; i++) {
+    if (K[4 * i] <= 0 || K[4 * i + 1] <= 0) {
+      set_error("focal lengths must be positive");
+      return TSDF_EDATASET;
+    }
+    args[i] = DepthArgs{depth[i], depth_dtype, rgb ? rgb[i] : nullptr, rgb_dtype, height, width,
+                        mem, make_frame(K + 4 * i, R + 9 * i, trans + 3 * i, tau, weight_cap)};
+  }
+  std::vector<IntegrationStats> st(n_frames);
+  int done = 0;
+  int s = integrate_depth_batch(T_(t), n_frames, args.data(), st.data(), &done);
+  for (int i = 0; i < n_frames; i++) memcpy(&stats[i], &st[i], sizeof(st[i]));
+  *n_done = done;
+  return s;
 }
 
 }  // extern "C"

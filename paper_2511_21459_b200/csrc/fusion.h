@@ -40,6 +40,14 @@ struct Table {
   Buf in0, in1, dray, dcol, ends, flags, new_list, touched, work, pairs, pairs_alt, cub_tmp,
       ray_len, ray_nhat, ray_src, ray_rgb, block_sums, lists, cand, mesh_scratch;
   Buf cand_l[kMaxLevels];
+  Buf batch, pyr;
+  Counters* hbatch = nullptr;  // pinned, hbatch_n entries
+  int hbatch_n = 0;
+  // merge-pass memo: stats are re-evaluated only for dirty blocks while the
+  // parameters are unchanged
+  bool merge_memo = false;
+  double memo_sigma = 0, memo_frac = 0, memo_w = 0;
+  int memo_all = 0;
   // kernel launch telemetry: launches of our kernels since creation
   uint64_t launches = 0;
   // optional per-kernel event timing (bench / profiling)
@@ -82,6 +90,16 @@ int table_create(int64_t n_hash, int32_t bucket, int32_t overflow, double block_
 int table_destroy(Table* t);
 int table_reset(Table* t);
 
+struct DepthArgs {
+  const void* depth;
+  int depth_dtype;
+  const void* rgb;
+  int rgb_dtype;
+  int H, W, mem;
+  Frame f;
+};
+int integrate_depth_batch(Table* T, int B, const DepthArgs* frames, IntegrationStats* st,
+                          int* n_done);
 int integrate_depth(Table* T, const void* depth, int depth_dtype, const void* rgb,
                     int rgb_dtype, int H, int W, int mem, const Frame& f,
                     IntegrationStats* st);

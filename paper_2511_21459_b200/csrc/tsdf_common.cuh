@@ -74,7 +74,21 @@ struct DevTable {
   int32_t n_levels;
   double edge;
   int32_t shard_rank, shard_world;
+  // blocks whose voxels changed since the last merge pass
+  uint32_t* dirty;       // per slot flag
+  uint32_t* dirty_list;  // slots, in first-dirtied order
+  unsigned long long* n_dirty;
   DevHeap heap[kMaxLevels];
+};
+
+// per-frame min/max pyramid of the measured ray distance (band cull)
+constexpr int kMaxPyr = 16;
+struct Pyramid {
+  float* lo;
+  float* hi;
+  int32_t n_levels;
+  int32_t w[kMaxPyr], h[kMaxPyr];
+  int64_t off[kMaxPyr];
 };
 
 // per-call device counters (one struct, read back once per call)
@@ -87,8 +101,8 @@ struct Counters {
   unsigned long long voxels_updated;
   unsigned long long observations;
   unsigned long long dda_cap;      // global lock-step cap (dda.py:63)
-  unsigned long long zmin_bits;    // positive doubles order like their bits
-  unsigned long long zmax_bits;
+  unsigned long long zmin_inv;     // max of ~bits(z): a zeroed struct is the identity
+  unsigned long long zmax_bits;    // positive doubles order like their bits
   unsigned long long candidates;
   unsigned long long merged;
   unsigned long long mesh_verts;

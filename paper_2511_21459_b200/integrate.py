@@ -110,6 +110,56 @@ def integrate_depth(table: HashTable, frame: DepthFrame, tau: float, archive=Non
     return _stats(st)
 
 
+def integrate_depth_batch(table: HashTable, frames, tau: float, archive=None,
+                          weight_cap: float = 0.0) -> list:
+    """Integrate the frames of one merge window with a single host sync.
+
+    Same result as calling ``integrate_depth`` on each frame in order (the
+    table only changes at merge boundaries outside this call); on an error
+    at frame i the later frames are not applied and the error is raised.
+    All frames must share size and dtypes.
+    """
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    _check_archive(archive)
+    frames = list(frames)
+    n = len(frames)
+    if n == 0:
+        return []
+    keep, dptrs, cptrs = [], [], []
+    ddt = cdt = mem = None
+    for f in frames:
+        p, dt, m, k = N.as_buffer(f.depth, (N.F64, N.F32))
+        keep.append(k)
+        if ddt is None:
+            ddt, mem = dt, m
+        if dt != ddt or m != mem or (f.height, f.width) != (frames[0].height, frames[0].width):
+            raise ValueError("integrate_depth_batch: frames must share size, dtype and memory kind")
+        dptrs.append(p)
+        if f.color is not None:
+            cp, ct, cm, ck = N.as_buffer(f.color, (N.F64, N.F32, N.U8))
+            keep.append(ck)
+            if cdt is None:
+                cdt = ct
+            if ct != cdt or cm != mem:
+                raise ValueError("integrate_depth_batch: colours must share dtype and memory kind")
+            cptrs.append(cp)
+    if cptrs and len(cptrs) != n:
+        raise ValueError("integrate_depth_batch: either every frame has colour or none")
+    K = np.concatenate([f.intrinsics.as_array() for f in frames])
+    R = np.concatenate([np.ascontiguousarray(f.pose.rotation, dtype=np.float64).reshape(9) for f in frames])
+    T = np.concatenate([np.ascontiguousarray(f.pose.translation, dtype=np.float64).reshape(3) for f in frames])
+    darr = (C.c_void_p * n)(*dptrs)
+    carr = (C.c_void_p * n)(*cptrs) if cptrs else None
+    st = (N.IntegrationStatsC * n)()
+    done = C.c_int32()
+    rc = N.lib().tsdf_integrate_depth_batch(table._h, n, darr, ddt, carr, cdt or 0,
+                                            frames[0].height, frames[0].width, mem, K, R, T,
+                                            float(tau), float(weight_cap), st, C.byref(done))
+    N.check(rc, "integrate_depth_batch")
+    return [_stats(s) for s in st]
+
+
 def integrate_pointcloud(table: HashTable, frame: PointCloudFrame, tau: float, archive=None,
                          weight_cap: float = 0.0) -> IntegrationStats:
     """Ray-based fusion of one point cloud (integrate.py:175-252)."""

@@ -343,3 +343,65 @@ def test_block_key_sharding_union_equals_single_gpu(world):
             a = rows[c]
             assert np.array_equal(a[0], ts[j]) and np.array_equal(a[1], w[j])
             assert np.array_equal(a[2], s2[j]) and np.array_equal(a[3], col[j])
+
+
+def test_depth_batch_equals_per_frame_and_oracle():
+    """integrate_depth_batch (one host sync per merge window) == per-frame calls == oracle."""
+    import paper_2511_21459_b200 as P
+    frames = P.synth.render_frames("room", 20, 160, 120, depth_dtype=np.float32,
+                                   color_dtype=np.uint8)
+    a = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000, 5000))
+    b = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000, 5000))
+    o = PU.OracleBackend(1000003, 0.04, (100000, 20000, 5000))
+    for w in range(2):
+        win = frames[10 * w:10 * (w + 1)]
+        sa = P.integrate_depth_batch(a, win, 0.015)
+        sb = [P.integrate_depth(b, f, 0.015) for f in win]
+        so = [o.depth(f, 0.015) for f in win]
+        assert [x.__dict__ for x in sa] == [x.__dict__ for x in sb]
+        assert [{k: getattr(x, k) for k in PU.STAT_KEYS} for x in sa] == so
+        ma = P.apply_merges(a, 2.5e-5, all_levels=True)
+        mb = P.apply_merges(b, 2.5e-5, all_levels=True)
+        mo = o.merge(2.5e-5, all_levels=True)
+        assert (ma.candidates, ma.merged) == (mb.candidates, mb.merged) == (mo["candidates"], mo["merged"])
+    ga = PU.GpuBackend.state(type("x", (), {"t": a})())
+    assert PU.state_digest(ga) == PU.state_digest(o.state())
+
+
+def test_depth_batch_capacity_error_stops_at_failing_frame():
+    import paper_2511_21459_b200 as P
+    frames = P.synth.render_frames("room", 4, 64, 48)
+    t = P.HashTable(100003, 10, 7, 0.08, (700, 10))
+    single = P.HashTable(100003, 10, 7, 0.08, (700, 10))
+    n_ok = 0
+    for f in frames:
+        try:
+            P.integrate_depth(single, f, 0.03)
+            n_ok += 1
+        except P.CapacityError:
+            break
+    assert n_ok < len(frames)
+    with pytest.raises(P.CapacityError):
+        P.integrate_depth_batch(t, frames, 0.03)
+    assert t.key_levels() == single.key_levels()
+
+
+def test_merge_memo_respects_parameter_changes():
+    """Dirty-block merge passes must equal full evaluation, including when the
+    parameters change between passes (then every block is re-evaluated)."""
+    spec = ("sphere", 30, 48, 36, 0.08, 0.03, (20000, 10000, 4000), 100003)
+    schedule = [(1e-6, False), (2.5e-4, False), (2.5e-4, True), (2.5e-3, True), (2.5e-3, True)]
+    results = {}
+    for name in ("gpu", "oracle"):
+        b = PU.BACKENDS[name](spec[6], spec[4], spec[5]) if False else None
+        from paper_2511_21459_b200 import synth
+        b = PU.BACKENDS[name](spec[7], spec[4], spec[6])
+        seq = synth.render_frames(spec[0], spec[1], spec[2], spec[3])
+        out = []
+        for i, f in enumerate(seq):
+            b.depth(f, spec[5])
+            if (i + 1) % 6 == 0:
+                sigma, al = schedule[(i + 1) // 6 - 1]
+                out.append(b.merge(sigma, all_levels=al))
+        results[name] = (out, PU.state_digest(b.state()))
+    assert results["gpu"] == results["oracle"]
