@@ -393,7 +393,6 @@ def test_merge_memo_respects_parameter_changes():
     schedule = [(1e-6, False), (2.5e-4, False), (2.5e-4, True), (2.5e-3, True), (2.5e-3, True)]
     results = {}
     for name in ("gpu", "oracle"):
-        b = PU.BACKENDS[name](spec[6], spec[4], spec[5]) if False else None
         from paper_2511_21459_b200 import synth
         b = PU.BACKENDS[name](spec[7], spec[4], spec[6])
         seq = synth.render_frames(spec[0], spec[1], spec[2], spec[3])
