@@ -209,6 +209,7 @@ def run_b200(args, wl, rank, world, dist, torch):
         P.apply_merges(table, wl["sigma"], all_levels=True)
     table.profile(True)
     table.kernel_times(reset=True)
+    table.work_totals(reset=True)
     launches0 = table.kernel_launches
     barrier()
     sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
@@ -229,6 +230,7 @@ def run_b200(args, wl, rank, world, dist, torch):
     barrier()
     launches = table.kernel_launches - launches0
     ktimes = table.kernel_times(reset=True)
+    work = table.work_totals(reset=True)
     table.profile(False)
     occ = [h.occupied for h in table.heaps]
     dev_ms = float(sum(step_ms))
@@ -307,7 +309,8 @@ def run_b200(args, wl, rank, world, dist, torch):
                    "l2": "256 MB L2 flush between timed steps (outside the events)",
                    "parallelism": f"block-key-hash shards x{world}" if world > 1 else "single GPU",
                    "blocks_live_end": occ, "merged_in_timed_region": merged,
-                   "work_units": {k: int(v) for k, v in B.items() if k in "PTAU"}},
+                   "work_units": {k: int(v) for k, v in B.items() if k in "PTAU"},
+                   "diagnostics": work},
         "e2e": {"value": round(e2e_value, 3), "unit": "Mpoints/s", "h2d_bytes_per_step": h2d // K,
                 "d2h_bytes_per_step": d2h // K},
         "roofline": {"bound": "hbm", "kernel": top_name, "achieved": round(achieved, 2),

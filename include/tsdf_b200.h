@@ -177,6 +177,10 @@ void tsdf_free(void *p);
  * stream while enabled; tsdf_profile_read returns {name, total ms, launches}
  * per kernel (names: name_stride bytes each). */
 int tsdf_profile_enable(tsdf_table *t, int32_t on);
+/* work totals since the last reset: [0] frames/scans, [1] touched blocks,
+ * [2] depth blocks kept by the band cull, [3] LiDAR near pairs,
+ * [4] sum of DDA lock-step caps */
+int tsdf_work_totals(tsdf_table *t, int64_t *out, int32_t reset);
 int tsdf_profile_read(tsdf_table *t, int32_t reset, int32_t max_entries, char *names,
                       int32_t name_stride, double *ms, int64_t *counts, int32_t *n_out);
 const char *tsdf_last_error(void);

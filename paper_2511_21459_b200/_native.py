@@ -106,6 +106,7 @@ def lib():
     L.tsdf_collapse_vertices.argtypes = [_ptr, _ptr, _ptr, i64, _ptr, i64, dbl, C.POINTER(MeshC)]
     L.tsdf_free.argtypes = [_ptr]
     L.tsdf_profile_enable.argtypes = [_ptr, i32]
+    L.tsdf_work_totals.argtypes = [_ptr, _i64p, i32]
     L.tsdf_profile_read.argtypes = [_ptr, i32, i32, C.c_char_p, i32, _f64p, _i64p, C.POINTER(i32)]
     _lib = L
     return L

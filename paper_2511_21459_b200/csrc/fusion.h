@@ -43,6 +43,9 @@ struct Table {
   Buf batch, pyr;
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
+  // work accounting for diagnostics: frames, touched, culled-in (depth
+  // update work items), near pairs, DDA cap sum
+  int64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   // merge-pass memo: stats are re-evaluated only for dirty blocks while the
   // parameters are unchanged
   bool merge_memo = false;

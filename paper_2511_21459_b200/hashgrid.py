@@ -192,6 +192,13 @@ class HashTable:
             out[nm] = (float(ms[i]), int(cnt[i]))
         return out
 
+    def work_totals(self, reset: bool = True) -> dict:
+        """Diagnostics: frames, touched blocks, band-cull survivors, near pairs."""
+        out = np.zeros(8, dtype=np.int64)
+        N.check(N.lib().tsdf_work_totals(self._h, out, int(bool(reset))), "work_totals")
+        return {"frames": int(out[0]), "touched": int(out[1]), "culled_in": int(out[2]),
+                "pairs": int(out[3]), "dda_cap_sum": int(out[4])}
+
     @property
     def kernel_launches(self) -> int:
         return int(N.lib().tsdf_kernel_launches(self._h))
