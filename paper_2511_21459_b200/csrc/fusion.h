@@ -40,7 +40,7 @@ struct Table {
   Buf in0, in1, dray, dcol, ends, flags, new_list, touched, work, pairs, pairs_alt, cub_tmp,
       ray_len, ray_nhat, ray_src, ray_rgb, block_sums, lists, cand, mesh_scratch;
   Buf cand_l[kMaxLevels];
-  Buf batch, pyr;
+  Buf batch, pyr, lidar_aux;
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
   // work accounting for diagnostics: frames, touched, culled-in (depth
