@@ -312,8 +312,8 @@ int tsdf_integrate_depth_batch(tsdf_table* t, int32_t n_frames, const void* cons
 
 extern "C" int tsdf_work_totals(tsdf_table* t, int64_t* out, int32_t reset) {
   NEED(t);
-  for (int i = 0; i < 8; i++) out[i] = T_(t)->acc[i];
+  for (int i = 0; i < 16; i++) out[i] = T_(t)->acc[i];
   if (reset)
-    for (int i = 0; i < 8; i++) T_(t)->acc[i] = 0;
+    for (int i = 0; i < 16; i++) T_(t)->acc[i] = 0;
   return TSDF_OK;
 }

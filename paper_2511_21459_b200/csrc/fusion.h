@@ -44,8 +44,9 @@ struct Table {
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
   // work accounting for diagnostics: frames, touched, culled-in (depth
-  // update work items), near pairs, DDA cap sum
-  int64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // update work items), near pairs, DDA cap sum, 8-voxel items, then the
+  // per-kernel Counters::diag fields
+  int64_t acc[16] = {};
   // merge-pass memo: stats are re-evaluated only for dirty blocks while the
   // parameters are unchanged
   bool merge_memo = false;

@@ -84,8 +84,7 @@ struct DevTable {
 // per-frame min/max pyramid of the measured ray distance (band cull)
 constexpr int kMaxPyr = 16;
 struct Pyramid {
-  float* lo;
-  float* hi;
+  float2* lh;  // (lo, hi) per cell
   int32_t n_levels;
   int32_t w[kMaxPyr], h[kMaxPyr];
   int64_t off[kMaxPyr];
@@ -108,6 +107,8 @@ struct Counters {
   unsigned long long mesh_verts;
   unsigned long long mesh_tris;
   unsigned long long aux0, aux1;
+  unsigned long long n_work2;      // depth: 8-voxel (level-2) work items
+  unsigned long long diag[6];      // work diagnostics (see fusion.cu kDiag*)
   uint32_t err;
   uint32_t pad;
   uint32_t free_top[kMaxLevels];

@@ -193,11 +193,15 @@ class HashTable:
         return out
 
     def work_totals(self, reset: bool = True) -> dict:
-        """Diagnostics: frames, touched blocks, band-cull survivors, near pairs."""
-        out = np.zeros(8, dtype=np.int64)
+        """Diagnostics: frames, touched blocks, near-filter / band-cull survivors
+        (blocks, 2x2x2 micro-bricks), voxels screened in FP32 and run on the
+        exact FP64 path, LiDAR near pairs, DDA cap sum."""
+        out = np.zeros(16, dtype=np.int64)
         N.check(N.lib().tsdf_work_totals(self._h, out, int(bool(reset))), "work_totals")
-        return {"frames": int(out[0]), "touched": int(out[1]), "culled_in": int(out[2]),
-                "pairs": int(out[3]), "dda_cap_sum": int(out[4])}
+        return {"frames": int(out[0]), "touched": int(out[1]), "block_pass": int(out[2]),
+                "pairs": int(out[3]), "dda_cap_sum": int(out[4]), "near_pass": int(out[6]),
+                "micro_pass": int(out[7]), "voxels_screened": int(out[8]),
+                "voxels_exact": int(out[9]), "subbrick_pass": int(out[10])}
 
     @property
     def kernel_launches(self) -> int:
