@@ -41,6 +41,7 @@ struct Table {
       ray_len, ray_nhat, ray_src, ray_rgb, block_sums, lists, cand, mesh_scratch;
   Buf cand_l[kMaxLevels];
   Buf batch, pyr, lidar_aux;
+  Buf dblk, dmicro, dexact;  // depth update work lists (blocks, micro-bricks, voxels)
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
   // work accounting for diagnostics: frames, touched, culled-in (depth

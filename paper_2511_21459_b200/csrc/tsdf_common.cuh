@@ -107,7 +107,7 @@ struct Counters {
   unsigned long long mesh_verts;
   unsigned long long mesh_tris;
   unsigned long long aux0, aux1;
-  unsigned long long n_work2;      // depth: 8-voxel (level-2) work items
+  unsigned long long n_sub, n_micro, n_exact;  // depth update work lists
   unsigned long long diag[6];      // work diagnostics (see fusion.cu kDiag*)
   uint32_t err;
   uint32_t pad;
