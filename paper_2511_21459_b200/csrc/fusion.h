@@ -42,6 +42,13 @@ struct Table {
   Buf cand_l[kMaxLevels];
   Buf batch, pyr, lidar_aux;
   Buf dblk, dmicro, dexact;  // depth update work lists (blocks, micro-bricks, voxels)
+  // depth batches overlap frame k+1's allocation (walk stream) with frame
+  // k's voxel update (main stream): per-parity copies of the frame scratch
+  // that both sides read
+  Buf in0b, in1b, drayb, flagsb, pyrb, touchedb;
+  cudaStream_t walk_stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_alloc[2] = {nullptr, nullptr}, ev_upd[2] = {nullptr, nullptr};
+  cudaStream_t prof_stream = nullptr;  // stream the profiling events go to (null: stream)
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
   // work accounting for diagnostics: frames, touched, culled-in (depth
