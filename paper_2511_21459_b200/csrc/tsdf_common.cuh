@@ -108,6 +108,7 @@ struct Counters {
   unsigned long long mesh_tris;
   unsigned long long aux0, aux1;
   unsigned long long n_sub, n_micro, n_exact;  // depth update work lists
+  unsigned long long tiles_done;                // k_depth_frame: finished tiles
   unsigned long long diag[6];      // work diagnostics (see fusion.cu kDiag*)
   uint32_t err;
   uint32_t pad;
