@@ -303,13 +303,25 @@ def run_b200(args, wl, rank, world, dist, torch):
     top_bytes = Bp[role] if role in Bp else Bp["path"]
     achieved = (top_bytes / top_n) / ((top_ms / top_n) * 1e-3) / 1e9 if top_ms > 0 else 0.0
     path_gbs = B["path"] / (dev_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, ncu = None, {}
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("traffic_per_launch", {}).get(top_name)
+            ncu = json.loads(prof.read_text())
+            traffic = ncu.get("traffic_per_launch", {}).get(top_name)
         except Exception:
-            traffic = None
+            traffic, ncu = None, {}
+    # the binding resource of the walk is instruction issue (FP64 DDA
+    # steps), not HBM: report its work rate beside the HBM roofline
+    secondary = None
+    if "k_dda_walk" in ktimes and work.get("dda_steps"):
+        w_ms, w_n = ktimes["k_dda_walk"]
+        steps = work["dda_steps"] / max(w_n, 1)
+        secondary = {"bound": "issue (FP64 DDA steps)", "kernel": "k_dda_walk",
+                     "dda_steps_per_launch": round(steps),
+                     "ms_per_launch": round(w_ms / max(w_n, 1), 4),
+                     "gsteps_per_s": round(steps / (w_ms / max(w_n, 1) * 1e-3) / 1e9, 3),
+                     "ncu_issue_active_frac": ncu.get("issue_active_frac", {}).get("k_dda_walk")}
     out = {
         "metric": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)" if wl["kind"] == "depth"
                   else "integrated Mpoints/s (128-beam LiDAR)",
@@ -335,7 +347,8 @@ def run_b200(args, wl, rank, world, dist, torch):
                      "path_achieved_gbs": round(path_gbs, 2),
                      "path_frac": round(path_gbs / peak, 5),
                      "bytes_per_launch": round(top_bytes / max(top_n, 1)),
-                     "ms_per_launch": round(top_ms / max(top_n, 1), 4)},
+                     "ms_per_launch": round(top_ms / max(top_n, 1), 4),
+                     "secondary": secondary},
         "kernels_ms": {k: [round(v[0], 3), v[1]] for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])},
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),

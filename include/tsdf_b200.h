@@ -182,8 +182,8 @@ int tsdf_profile_enable(tsdf_table *t, int32_t on);
  * [3] LiDAR near pairs, [4] sum of DDA lock-step caps, [5] reserved,
  * [6] depth blocks passing the near filter, [7] 2x2x2 micro-bricks kept by
  * the band cull, [8] voxels screened (FP32), [9] voxels on the exact FP64
- * path, [10] level-0 4x4x4 sub-bricks kept by the band cull, [11..15]
- * reserved */
+ * path, [10] level-0 4x4x4 sub-bricks kept by the band cull, [11] DDA
+ * steps walked, [12..15] reserved */
 int tsdf_work_totals(tsdf_table *t, int64_t *out, int32_t reset);
 int tsdf_profile_read(tsdf_table *t, int32_t reset, int32_t max_entries, char *names,
                       int32_t name_stride, double *ms, int64_t *counts, int32_t *n_out);

@@ -201,7 +201,8 @@ class HashTable:
         return {"frames": int(out[0]), "touched": int(out[1]), "block_pass": int(out[2]),
                 "pairs": int(out[3]), "dda_cap_sum": int(out[4]), "near_pass": int(out[6]),
                 "micro_pass": int(out[7]), "voxels_screened": int(out[8]),
-                "voxels_exact": int(out[9]), "subbrick_pass": int(out[10])}
+                "voxels_exact": int(out[9]), "subbrick_pass": int(out[10]),
+                "dda_steps": int(out[11])}
 
     @property
     def kernel_launches(self) -> int:
