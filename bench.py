@@ -13,8 +13,10 @@ API from pinned host buffers (H2D inside the timed region).
                     [--workload room|lidar]
 
 Multi-GPU (torchrun, one rank per GPU): block-key-hash sharding -- every
-rank integrates the same frames and owns 1/N of the blocks (strong
-scaling of a fixed frame stream); time = max over ranks.
+rank sees the same frames and owns 1/N of the blocks; depth frames split
+the full-ray DDA across ranks and route the keys to their owners with one
+all-to-all per frame (strong scaling of a fixed frame stream); time = max
+over ranks.
 """
 from __future__ import annotations
 
@@ -94,6 +96,7 @@ class ClockSampler:
         self.t.join(timeout=10)
 
     def summary(self):
+        self.rows = [r for r in self.rows if len(r) >= 6]  # drop nvidia-smi error lines
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -149,9 +152,24 @@ def integrate(P, t, wl, fr, device=None):
     return P.integrate_pointcloud(t, f, wl["tau"])
 
 
+_MULTI = {}  # set under torchrun: {"dist", "torch", "device"} for ray-sharded depth frames
+
+
 def window(P, t, wl, frs, dev=None):
     """One merge window through the public API: depth frames go through
-    integrate_depth_batch (one host sync per window), scans per scan."""
+    integrate_depth_batch (one host sync per window), scans per scan.  On
+    N > 1 GPUs depth frames use ray-sharded allocation: each rank walks 1/N
+    of the rays, one all-to-all routes the block keys to their owners, and
+    each rank updates the blocks it owns (sharding.integrate_depth_raysharded)."""
+    if wl["kind"] == "depth" and _MULTI:
+        from paper_2511_21459_b200.sharding import integrate_depth_raysharded
+        out = []
+        for i, fr in enumerate(frs):
+            f = P.DepthFrame(depth=fr[0] if dev is None else dev[i][0], intrinsics=fr[3], pose=fr[2],
+                             color=fr[1] if dev is None else dev[i][1])
+            out.append(integrate_depth_raysharded(t, f, wl["tau"], _MULTI["dist"], _MULTI["torch"],
+                                                  device=_MULTI["device"]))
+        return out
     if wl["kind"] == "depth":
         fs = [P.DepthFrame(depth=fr[0] if dev is None else dev[i][0], intrinsics=fr[3], pose=fr[2],
                            color=fr[1] if dev is None else dev[i][1]) for i, fr in enumerate(frs)]
@@ -177,10 +195,12 @@ KERNEL_ROLE = {"k_depth_update": "update", "k_lidar_update": "update", "k_dda_wa
 
 def run_b200(args, wl, rank, world, dist, torch):
     import paper_2511_21459_b200 as P
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
     shard = (rank, world) if world > 1 else None
+    if world > 1:
+        _MULTI.update(dist=dist, torch=torch, device=dev)
     W, K = args.warmup, args.steps
     nfr = FRAMES_PER_STEP * (W + 2 * K)  # warm-up, timed, then profiled windows
     t0 = time.time()
@@ -209,7 +229,7 @@ def run_b200(args, wl, rank, world, dist, torch):
         P.apply_merges(table, wl["sigma"], all_levels=True)
     launches0 = table.kernel_launches
     barrier()
-    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    sampler = ClockSampler(dev.index)
     with sampler:
         for s in range(K):
             flush.fill_(s & 0xFF)  # L2 flush between timed steps (outside the events)
@@ -414,6 +434,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="room", choices=list(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the multi-rank path with ranks sharing one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -428,8 +450,8 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
+        dist.init_process_group(args.dist_backend)
     out = run_b200(args, wl, rank, world, dist, torch)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:

@@ -96,6 +96,29 @@ int tsdf_integrate_depth(tsdf_table *t, const void *depth, int32_t depth_dtype, 
                          const double *K, const double *R, const double *trans, double tau,
                          double weight_cap, tsdf_integration_stats *stats);
 
+/* Ray-sharded depth integration for block-key-hash shards (
+ * the multi-GPU split of integrate.py:255-342).  Step 1 (walk): this rank
+ * walks the tiles of rays t with t % ray_world == ray_rank and writes every
+ * block key it meets once (packed, 21 bits per axis) to its owner's bucket:
+ * buckets is DEVICE memory [shard_world][bucket_cap], counts (host,
+ * shard_world entries) receives the per-owner key counts; stats gets the
+ * rank-invariant fields (measurements, skipped_invalid).  The caller
+ * exchanges buckets with an all-to-all.  Step 2 (keys): the keys this rank
+ * owns, gathered from every rank (DEVICE memory, duplicates allowed), are
+ * inserted -- touched once each --, new blocks committed, and the voxel
+ * update of the same frame runs; stats gets the block-partitioned fields.
+ * The frame's buffers (and a device-resident colour image) must stay valid
+ * until step 2 returns.  ray_world == 1 with an unsharded table equals
+ * tsdf_integrate_depth. */
+int tsdf_integrate_depth_walk(tsdf_table *t, const void *depth, int32_t depth_dtype,
+                              const void *rgb, int32_t rgb_dtype, int32_t height, int32_t width,
+                              int32_t mem, const double *K, const double *R, const double *trans,
+                              double tau, double weight_cap, int32_t ray_rank, int32_t ray_world,
+                              uint64_t *buckets, int64_t bucket_cap, int64_t *counts,
+                              tsdf_integration_stats *stats);
+int tsdf_integrate_depth_keys(tsdf_table *t, const uint64_t *keys, int64_t n,
+                              tsdf_integration_stats *stats);
+
 /* n_frames depth frames of one merge window (same size/dtypes), enqueued
  * back to back with one host synchronisation.  Per-frame K (4), R (9) and
  * trans (3) are packed consecutively.  Semantically identical to calling

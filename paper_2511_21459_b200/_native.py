@@ -77,6 +77,10 @@ def lib():
     L.tsdf_integrate_depth_batch.argtypes = [_ptr, i32, _ptr, i32, _ptr, i32, i32, i32, i32,
                                              _f64p, _f64p, _f64p, dbl, dbl,
                                              C.POINTER(IntegrationStatsC), C.POINTER(i32)]
+    L.tsdf_integrate_depth_walk.argtypes = [_ptr, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p,
+                                            _f64p, _f64p, dbl, dbl, i32, i32, _ptr, i64, _i64p,
+                                            C.POINTER(IntegrationStatsC)]
+    L.tsdf_integrate_depth_keys.argtypes = [_ptr, _ptr, i64, C.POINTER(IntegrationStatsC)]
     L.tsdf_integrate_points.argtypes = [_ptr, _ptr, i32, _ptr, i32, i64, i32, _f64p, _f64p, dbl,
                                         dbl, C.POINTER(IntegrationStatsC)]
     L.tsdf_allocate_for_measurement.argtypes = [_ptr, _f64p, _f64p, dbl, _i64p, i64,

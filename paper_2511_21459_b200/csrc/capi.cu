@@ -93,6 +93,47 @@ int tsdf_integrate_depth(tsdf_table* t, const void* depth, int32_t depth_dtype, 
   return s;
 }
 
+int tsdf_integrate_depth_walk(tsdf_table* t, const void* depth, int32_t depth_dtype,
+                              const void* rgb, int32_t rgb_dtype, int32_t height, int32_t width,
+                              int32_t mem, const double* K, const double* R, const double* trans,
+                              double tau, double weight_cap, int32_t ray_rank, int32_t ray_world,
+                              uint64_t* buckets, int64_t bucket_cap, int64_t* counts,
+                              tsdf_integration_stats* stats) {
+  NEED(t);
+  if (depth_dtype < 0 || depth_dtype > 3 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  if (K[0] <= 0 || K[1] <= 0) {
+    set_error("focal lengths must be positive");
+    return TSDF_EDATASET;
+  }
+  if (bucket_cap <= 0) {
+    set_error("bucket_cap must be positive");
+    return TSDF_EVALUE;
+  }
+  IntegrationStats st;
+  DepthArgs a{depth, depth_dtype, rgb, rgb_dtype, height, width, mem,
+              make_frame(K, R, trans, tau, weight_cap)};
+  int s = integrate_depth_walk(T_(t), a, ray_rank, ray_world, buckets, (uint64_t)bucket_cap, counts,
+                               &st);
+  memcpy(stats, &st, sizeof(st));
+  return s;
+}
+
+int tsdf_integrate_depth_keys(tsdf_table* t, const uint64_t* keys, int64_t n,
+                              tsdf_integration_stats* stats) {
+  NEED(t);
+  if (n < 0 || (n > 0 && !keys)) {
+    set_error("invalid key list");
+    return TSDF_EVALUE;
+  }
+  IntegrationStats st;
+  int s = integrate_depth_keys(T_(t), keys, n, &st);
+  memcpy(stats, &st, sizeof(st));
+  return s;
+}
+
 int tsdf_integrate_points(tsdf_table* t, const void* xyz, int32_t xyz_dtype, const void* rgb,
                           int32_t rgb_dtype, int64_t n, int32_t mem, const double* R,
                           const double* trans, double tau, double weight_cap,

@@ -25,6 +25,13 @@ struct ProfAcc {
   int64_t count = 0;
 };
 
+struct Frame {
+  double fx, fy, cx, cy;
+  double R[9];
+  double t[3];
+  double tau, weight_cap;
+};
+
 struct Table {
   DevTable d{};
   uint32_t* free_top = nullptr;  // device [kMaxLevels]
@@ -49,6 +56,18 @@ struct Table {
   cudaStream_t walk_stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_alloc[2] = {nullptr, nullptr}, ev_upd[2] = {nullptr, nullptr};
   cudaStream_t prof_stream = nullptr;  // stream the profiling events go to (null: stream)
+  // ray-sharded allocation (multi-GPU): per-frame "emitted" key set and the
+  // frame state kept between the walk call and the keys call
+  Buf fset;
+  struct ShardedFrame {
+    bool ready = false;
+    int H = 0, W = 0, rgb_dtype = 0;
+    const void* rgb = nullptr;  // device colour of the frame (staged or caller-owned)
+    Counters* c = nullptr;
+    uint32_t* abort_word = nullptr;
+    double f[20];               // FrameDev image
+  } shf;
+  Frame shf_frame{};
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
   // work accounting for diagnostics: frames, touched, culled-in (depth
@@ -85,12 +104,6 @@ struct MergeStats {
   int64_t candidates, merged;
 };
 
-struct Frame {
-  double fx, fy, cx, cy;
-  double R[9];
-  double t[3];
-  double tau, weight_cap;
-};
 
 void set_error(const std::string& msg);
 const char* last_error();
@@ -112,6 +125,10 @@ struct DepthArgs {
 };
 int integrate_depth_batch(Table* T, int B, const DepthArgs* frames, IntegrationStats* st,
                           int* n_done);
+int integrate_depth_walk(Table* T, const DepthArgs& a, int ray_rank, int ray_world,
+                         uint64_t* buckets, uint64_t bucket_cap, int64_t* counts,
+                         IntegrationStats* st);
+int integrate_depth_keys(Table* T, const uint64_t* keys, int64_t n, IntegrationStats* st);
 int integrate_depth(Table* T, const void* depth, int depth_dtype, const void* rgb,
                     int rgb_dtype, int H, int W, int mem, const Frame& f,
                     IntegrationStats* st);

@@ -51,6 +51,7 @@ enum ErrFlag : uint32_t {
   kErrPairOverflow = 8u,    // (ray, block) pair buffer too small
   kErrTableFull = 16u,      // hash slots exhausted
   kErrMeshOverflow = 32u,   // mesh output buffers too small
+  kErrShardRoute = 64u,     // a key reached a shard that does not own it
 };
 
 struct DevHeap {

@@ -205,6 +205,11 @@ class HashTable:
                 "dda_steps": int(out[11])}
 
     @property
+    def slots(self) -> int:
+        """Device hash-table slots (the bound on distinct blocks one call can touch)."""
+        return int(N.lib().tsdf_table_slots(self._h))
+
+    @property
     def kernel_launches(self) -> int:
         return int(N.lib().tsdf_kernel_launches(self._h))
 

@@ -110,6 +110,57 @@ def integrate_depth(table: HashTable, frame: DepthFrame, tau: float, archive=Non
     return _stats(st)
 
 
+def integrate_depth_walk(table: HashTable, frame: DepthFrame, tau: float, ray_rank: int,
+                         ray_world: int, buckets, weight_cap: float = 0.0):
+    """Step 1 of ray-sharded depth integration (multi-GPU).
+
+    Walks this rank's share of the rays (16x16-pixel tiles t with
+    t % ray_world == ray_rank) with the reference's full-ray DDA
+    (integrate.py:282-290) and writes each block key it meets once into the
+    bucket of the shard that owns it.  `buckets` is a CUDA int64 array of
+    shape (shard_world, cap).  Returns (stats with the rank-invariant fields,
+    per-owner key counts).  The frame must stay alive until
+    integrate_depth_keys returns."""
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    dptr, ddt, dmem, _keep_d = N.as_buffer(frame.depth, (N.F64, N.F32))
+    cptr, cdt, cmem, _keep_c = (None, 0, dmem, None)
+    if frame.color is not None:
+        cptr, cdt, cmem, _keep_c = N.as_buffer(frame.color, (N.F64, N.F32, N.U8))
+        if cmem != dmem:
+            raise ValueError("depth and colour must both live on the host or both on the device")
+    cai = getattr(buckets, "__cuda_array_interface__", None)
+    if cai is None or len(cai["shape"]) != 2 or np.dtype(cai["typestr"]).itemsize != 8:
+        raise ValueError("buckets must be a 2-D 64-bit CUDA array (shard_world, cap)")
+    world, cap = (int(x) for x in cai["shape"])
+    counts = np.zeros(max(world, 1), dtype=np.int64)
+    R, t = _pose(frame.pose)
+    st = N.IntegrationStatsC()
+    N.check(N.lib().tsdf_integrate_depth_walk(table._h, dptr, ddt, cptr, cdt, frame.height,
+                                              frame.width, dmem, frame.intrinsics.as_array(), R, t,
+                                              float(tau), float(weight_cap), int(ray_rank),
+                                              int(ray_world), cai["data"][0], cap, counts,
+                                              C.byref(st)),
+            "integrate_depth_walk")
+    return _stats(st), counts[:world]
+
+
+def integrate_depth_keys(table: HashTable, keys, n: int = None) -> IntegrationStats:
+    """Step 2 of ray-sharded depth integration: insert the block keys this
+    shard owns (a CUDA int64 array gathered from every rank; duplicates are
+    fine), commit the new blocks and run the voxel update of the frame given
+    to the preceding integrate_depth_walk.  Returns the block-partitioned
+    stats (blocks_allocated, blocks_touched, voxels_updated, observations)."""
+    cai = getattr(keys, "__cuda_array_interface__", None)
+    if cai is None or np.dtype(cai["typestr"]).itemsize != 8:
+        raise ValueError("keys must be a 64-bit CUDA array")
+    n = int(np.prod(cai["shape"])) if n is None else int(n)
+    st = N.IntegrationStatsC()
+    N.check(N.lib().tsdf_integrate_depth_keys(table._h, cai["data"][0] if n else None, n,
+                                              C.byref(st)), "integrate_depth_keys")
+    return _stats(st)
+
+
 def integrate_depth_batch(table: HashTable, frames, tau: float, archive=None,
                           weight_cap: float = 0.0) -> list:
     """Integrate the frames of one merge window with a single host sync.

@@ -2,11 +2,18 @@
 
 owner(key) = (splitmix64(packed key) >> 32) mod G, decorrelated from the
 table's slot hash.  Every rank receives the whole frame (NCCL broadcast over
-NVLink from rank 0), traverses all rays, and allocates / updates only the
-blocks it owns; merges are rank-local (a block's merge depends only on its
-own voxels), so the union over ranks equals the single-GPU table
-bit-for-bit.  Counters that partition by block are summed with one
-all-reduce; per-frame counters (measurements, skipped) are rank-invariant.
+NVLink from rank 0) and allocates / updates only the blocks it owns; merges
+are rank-local (a block's merge depends only on its own voxels), so the union
+over ranks equals the single-GPU table bit-for-bit.  Counters that partition
+by block are summed with one all-reduce; per-frame counters (measurements,
+skipped) are rank-invariant.
+
+Depth frames use ray-sharded allocation: rank r walks 1/G of the rays
+(integrate_depth_walk), the per-owner key buckets go through one
+all-to-all, and each rank inserts and updates the keys it owns
+(integrate_depth_keys) -- the full-ray DDA is split G ways instead of
+replicated.  LiDAR scans walk every ray on every rank and keep the blocks
+they own (the (block, ray) pairs would need the ray data exchanged too).
 """
 from __future__ import annotations
 
@@ -59,7 +66,14 @@ class ShardedFusion:
         return broadcast_frame(frame, self.dist, self.torch, self.group, self.device)
 
     def integrate_frame(self, frame):
+        from .geometry import DepthFrame
         f = self.broadcast_frame(frame) if self.world > 1 else frame
+        if self.world > 1 and isinstance(f, DepthFrame):
+            cfg = self.engine.config
+            st = integrate_depth_raysharded(self.engine.table, f, cfg.tau, self.dist, self.torch,
+                                            self.group, self.device, cfg.weight_cap)
+            self.engine.frame_index += 1
+            return st
         st = self.engine.integrate_frame(f)
         return combine_stats(st, self.dist, self.torch, self.group, self.device)
 
@@ -112,10 +126,51 @@ def broadcast_frame(frame, dist, torch, group=None, device=None):
 def combine_stats(st, dist, torch, group=None, device=None):
     """Sum the block-partitioned counters over ranks (one all-reduce)."""
     from .integrate import IntegrationStats
-    v = torch.tensor([getattr(st, k) for k in PARTITIONED], dtype=torch.int64, device=device)
+    host = dist.get_backend(group) == "gloo"
+    v = torch.tensor([getattr(st, k) for k in PARTITIONED], dtype=torch.int64,
+                     device="cpu" if host else device)
     dist.all_reduce(v, group=group)
     out = IntegrationStats(**{k: getattr(st, k) for k in INVARIANT})
     for k, x in zip(PARTITIONED, v.tolist()):
         setattr(out, k, int(x))
     out.warnings = list(st.warnings)
     return out
+
+
+def exchange_keys(buckets, counts, dist, torch, group=None, device=None):
+    """All-to-all of per-owner key buckets: bucket o of this rank goes to rank
+    o; returns the concatenation of every rank's bucket for this rank."""
+    world = dist.get_world_size(group)
+    # gloo (CPU tests, or several ranks sharing one GPU) exchanges host copies
+    host = dist.get_backend(group) == "gloo"
+    cdev = "cpu" if host else device
+    send_counts = torch.as_tensor(np.asarray(counts, dtype=np.int64), device=cdev)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    sc = [int(x) for x in np.asarray(counts)]
+    rc = [int(x) for x in recv_counts.tolist()]
+    send = torch.cat([buckets[o, :sc[o]] for o in range(world)])
+    out_dev = send.device
+    if host:
+        send = send.cpu()
+    recv = torch.empty(sum(rc), dtype=send.dtype, device=send.device)
+    dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc, group=group)
+    return recv.to(out_dev)
+
+
+def integrate_depth_raysharded(table, frame, tau, dist, torch, group=None, device=None,
+                               weight_cap: float = 0.0):
+    """One depth frame on a block-key-hash shard with the rays split across
+    ranks: walk this rank's rays -> all-to-all of the owned keys -> insert,
+    commit and update this rank's blocks -> one all-reduce of the
+    block-partitioned counters."""
+    from .integrate import integrate_depth_keys, integrate_depth_walk
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buckets = torch.empty((world, table.slots), dtype=torch.int64, device=device)
+    st1, counts = integrate_depth_walk(table, frame, tau, rank, world, buckets, weight_cap)
+    recv = exchange_keys(buckets, counts, dist, torch, group, device)
+    st2 = integrate_depth_keys(table, recv)
+    for k in INVARIANT:
+        setattr(st2, k, getattr(st1, k))
+    st2.warnings = list(st1.warnings)
+    return combine_stats(st2, dist, torch, group, device)

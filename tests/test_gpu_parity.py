@@ -345,6 +345,81 @@ def test_block_key_sharding_union_equals_single_gpu(world):
             assert np.array_equal(a[2], s2[j]) and np.array_equal(a[3], col[j])
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_ray_sharded_allocation_union_equals_single_gpu(world):
+    """Ray-sharded multi-GPU allocation on one device: `world`
+    shard tables each walk 1/world of the rays, emit the keys they see into
+    per-owner buckets, the buckets are exchanged (concatenated per owner, as
+    all-to-all does), and each shard inserts + updates its own keys.  The
+    union of shards equals the single table bit-for-bit, the partitioned
+    counters sum to its counters, and the invariant ones agree."""
+    import torch
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200.sharding import INVARIANT, PARTITIONED, owner_of_coords
+    frames = P.synth.render_frames("room", 20, 160, 120, depth_dtype=np.float32,
+                                   color_dtype=np.uint8)
+    full = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000))
+    shards = []
+    for r in range(world):
+        t = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000))
+        if world > 1:
+            t.set_shard(r, world)
+        shards.append(t)
+    dev = torch.device("cuda", 0)
+    buckets = [torch.zeros((world, t.slots), dtype=torch.int64, device=dev) for t in shards]
+    for i, f in enumerate(frames):
+        s_full = P.integrate_depth(full, f, 0.015)
+        walks = []
+        for r, t in enumerate(shards):
+            walks.append(P.integrate_depth_walk(t, f, 0.015, r, world, buckets[r]))
+        parts = []
+        for o, t in enumerate(shards):
+            keys = torch.cat([buckets[r][o, :int(walks[r][1][o])] for r in range(world)])
+            # the key call completes each shard's frame; the walk state is per table
+            parts.append(P.integrate_depth_keys(t, keys))
+        for k in PARTITIONED:
+            assert sum(getattr(p, k) for p in parts) == getattr(s_full, k), (i, k)
+        for k in INVARIANT:
+            assert all(getattr(w[0], k) == getattr(s_full, k) for w in walks), (i, k)
+        if (i + 1) % 10 == 0:
+            m = P.apply_merges(full, 2.5e-5).merged
+            assert sum(P.apply_merges(t, 2.5e-5).merged for t in shards) == m
+    for level in range(2):
+        co, _, ts, w, s2, col = full.export_level(level)
+        rows = {}
+        for r, t in enumerate(shards):
+            c2, _, t2, w2, s22, col2 = t.export_level(level)
+            assert np.all(owner_of_coords(c2, world) == r)
+            for j, c in enumerate(map(tuple, c2.tolist())):
+                rows[c] = (t2[j], w2[j], s22[j], col2[j])
+        assert set(rows) == set(map(tuple, co.tolist()))
+        for j, c in enumerate(map(tuple, co.tolist())):
+            a = rows[c]
+            assert np.array_equal(a[0], ts[j]) and np.array_equal(a[1], w[j])
+            assert np.array_equal(a[2], s2[j]) and np.array_equal(a[3], col[j])
+
+
+def test_ray_sharded_keys_need_walk_and_routing():
+    """integrate_depth_keys without a preceding walk is an error, and a key
+    routed to a shard that does not own it is rejected."""
+    import torch
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200.sharding import owner_of_keys, pack_keys
+    t = P.HashTable(100003, 10, 7, 0.04, (10000, 1000))
+    t.set_shard(0, 2)
+    dev = torch.device("cuda", 0)
+    with pytest.raises(ValueError):
+        P.integrate_depth_keys(t, torch.zeros(1, dtype=torch.int64, device=dev))
+    f = P.synth.render_frames("room", 1, 64, 48, depth_dtype=np.float32)[0]
+    b = torch.zeros((2, t.slots), dtype=torch.int64, device=dev)
+    P.integrate_depth_walk(t, f, 0.015, 0, 1, b)
+    coords = np.array([[i, 0, 0] for i in range(64)])
+    keys = pack_keys(coords)
+    foreign = keys[owner_of_keys(keys, 2) == 1][:1].astype(np.int64)
+    with pytest.raises(ValueError):
+        P.integrate_depth_keys(t, torch.as_tensor(foreign, device=dev))
+
+
 def test_depth_batch_equals_per_frame_and_oracle():
     """integrate_depth_batch (one host sync per merge window) == per-frame calls == oracle."""
     import paper_2511_21459_b200 as P

@@ -73,3 +73,70 @@ def test_two_rank_partition_and_reduce():
         assert vox0 == vox1 == st0["voxels_updated"]   # shard sums == whole frame
         assert meas0 == st0["measurements"]
         assert touched0 == touched1 == live0   # every live block owned exactly once
+
+
+def _exchange_worker(rank, world, port, q):
+    """Ray-sharded key exchange (sharding.exchange_keys) with the oracle as
+    the walk: rank r takes the tiles t % world == r of a frame, emits the
+    blocks its rays cross (the oracle's DDA rows) into per-owner buckets,
+    and after the all-to-all every rank must hold exactly the frame's keys
+    that it owns."""
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "tests"))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_21459_b200 import synth
+    from paper_2511_21459_b200.sharding import exchange_keys, owner_of_keys, pack_keys
+    from oracle.oracle import oracle_dda_blocks_batch
+    f = synth.render_frames("room", 1, 48, 32, depth_dtype=np.float32)[0]
+    H, W = f.depth.shape
+    # back-project + segment ends as integrate.py:278-286 (host numpy, small case)
+    v, u = np.mgrid[0:H, 0:W]
+    z = f.depth.astype(np.float64)
+    ok = np.isfinite(z) & (z > 0)
+    k = f.intrinsics
+    pc = np.stack([(u - k.cx) / k.fx * z, (v - k.cy) / k.fy * z, z], -1)[ok]
+    tile = ((v // 16) * ((W + 15) // 16) + (u // 16))[ok]
+    pw = pc @ f.pose.rotation.T + f.pose.translation
+    ray = pw - f.pose.translation
+    e = pw + 0.015 * ray / np.linalg.norm(ray, axis=1)[:, None]
+    mine = tile % world == rank
+    o = np.repeat(f.pose.translation[None], len(e), 0)
+    # one lock-step batch over the whole frame (its global cap), then this
+    # rank's rays' rows
+    ids, rows_all = oracle_dda_blocks_batch(o, e, 0.04)
+    rows_mine = rows_all[mine[ids]]
+    keys = np.unique(pack_keys(rows_mine))
+    own = owner_of_keys(keys, world)
+    cap = max(1, len(keys))
+    buckets = torch.zeros((world, cap), dtype=torch.int64)
+    counts = np.zeros(world, dtype=np.int64)
+    for r in range(world):
+        sel = keys[own == r].astype(np.int64)
+        buckets[r, :len(sel)] = torch.from_numpy(sel)
+        counts[r] = len(sel)
+    recv = exchange_keys(buckets, counts, dist, torch)
+    got = set(np.unique(recv.numpy().astype(np.uint64)).tolist())
+    allk = np.unique(pack_keys(rows_all))
+    want = set(allk[owner_of_keys(allk, world) == rank].tolist())
+    q.put((rank, got == want, len(want)))
+    dist.destroy_process_group()
+
+
+def test_two_rank_ray_sharded_key_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (ok, n)) for r, ok, n in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok and n > 0 for ok, n in res.values())
