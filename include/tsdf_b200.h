@@ -169,6 +169,32 @@ int tsdf_read_block(tsdf_table *t, const int64_t *coord, int32_t *level, double 
                     double *weight, double *s2, float *color);
 int tsdf_write_block(tsdf_table *t, const int64_t *coord, const double *tsdf,
                      const double *weight, const double *s2, const float *color);
+/* The distinct block keys (packed, 21 bits per axis, sorted) that the
+ * allocation of a depth frame / a point scan would touch -- the reference's
+ * unique DDA coordinates (integrate.py:203, :289) -- without changing the
+ * table.  The capacity tier uses them to stream archived blocks back in
+ * before integrating (integrate.py:122-140). */
+int tsdf_depth_keys(tsdf_table *t, const void *depth, int32_t depth_dtype, int32_t height,
+                    int32_t width, int32_t mem, const double *K, const double *R, const double *trans,
+                    double tau, uint64_t *keys, int64_t cap, int64_t *n_out);
+int tsdf_scan_keys(tsdf_table *t, const void *xyz, int32_t xyz_dtype, int64_t n, int32_t mem,
+                   const double *R, const double *trans, double tau, uint64_t *keys, int64_t cap,
+                   int64_t *n_out);
+
+/* Capacity tier (streaming.py stream_out / stream_in, formats.py
+ * save_map / load_map): bulk transfer of n blocks of one level in the
+ * reference's BlockPayload layout -- tsdf, weight, s2 f64 [n][nvox], colour
+ * f32 [n][nvox][3], host memory.  evict removes the blocks (payload out,
+ * heap slots freed, TSDF_ENOTFOUND if one is not live at that level, table
+ * untouched); import inserts them at `level` with their payload
+ * (TSDF_EVALUE if one is already live, TSDF_ECAPACITY on heap / chain
+ * exhaustion; either way the table is left as before the call). */
+int tsdf_evict_level(tsdf_table *t, int32_t level, const int64_t *coords, int64_t n, double *tsdf,
+                     double *weight, double *s2, float *color);
+int tsdf_import_level(tsdf_table *t, int32_t level, const int64_t *coords, int64_t n,
+                      const double *tsdf, const double *weight, const double *s2,
+                      const float *color);
+
 /* BlockHeap.occupied for one level */
 int tsdf_live_count(tsdf_table *t, int32_t level, int64_t *n);
 /* all live blocks of a level in canonical (x, y, z) order with their

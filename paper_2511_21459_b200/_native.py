@@ -94,6 +94,12 @@ def lib():
     L.tsdf_remove.argtypes = [_ptr, _i64p, C.POINTER(i32), _ptr, _ptr, _ptr, _ptr]
     L.tsdf_read_block.argtypes = [_ptr, _i64p, C.POINTER(i32), _ptr, _ptr, _ptr, _ptr]
     L.tsdf_write_block.argtypes = [_ptr, _i64p, _ptr, _ptr, _ptr, _ptr]
+    L.tsdf_depth_keys.argtypes = [_ptr, _ptr, i32, i32, i32, i32, _f64p, _f64p, _f64p, dbl, _ptr,
+                                  i64, C.POINTER(i64)]
+    L.tsdf_scan_keys.argtypes = [_ptr, _ptr, i32, i64, i32, _f64p, _f64p, dbl, _ptr, i64,
+                                 C.POINTER(i64)]
+    L.tsdf_evict_level.argtypes = [_ptr, i32, _i64p, i64, _ptr, _ptr, _ptr, _ptr]
+    L.tsdf_import_level.argtypes = [_ptr, i32, _i64p, i64, _ptr, _ptr, _ptr, _ptr]
     L.tsdf_live_count.argtypes = [_ptr, i32, C.POINTER(i64)]
     L.tsdf_export_level.argtypes = [_ptr, i32, i64, _ptr, _ptr, _ptr, _ptr, _ptr, _ptr,
                                     C.POINTER(i64)]

@@ -134,6 +134,49 @@ int tsdf_integrate_depth_keys(tsdf_table* t, const uint64_t* keys, int64_t n,
   return s;
 }
 
+int tsdf_depth_keys(tsdf_table* t, const void* depth, int32_t depth_dtype, int32_t height,
+                    int32_t width, int32_t mem, const double* K, const double* R, const double* trans,
+                    double tau, uint64_t* keys, int64_t cap, int64_t* n_out) {
+  NEED(t);
+  if (depth_dtype < 0 || depth_dtype > 3) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  if (K[0] <= 0 || K[1] <= 0) {
+    set_error("focal lengths must be positive");
+    return TSDF_EDATASET;
+  }
+  DepthArgs a{depth, depth_dtype, nullptr, 0, height, width, mem, make_frame(K, R, trans, tau, 0.0)};
+  return depth_keys(T_(t), a, keys, cap, n_out);
+}
+
+int tsdf_scan_keys(tsdf_table* t, const void* xyz, int32_t xyz_dtype, int64_t n, int32_t mem,
+                   const double* R, const double* trans, double tau, uint64_t* keys, int64_t cap,
+                   int64_t* n_out) {
+  NEED(t);
+  if (xyz_dtype < 0 || xyz_dtype > 1) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  *n_out = 0;
+  if (n == 0) return TSDF_OK;
+  return scan_keys(T_(t), xyz, xyz_dtype, n, mem, make_frame(nullptr, R, trans, tau, 0.0), keys, cap,
+                   n_out);
+}
+
+int tsdf_evict_level(tsdf_table* t, int32_t level, const int64_t* coords, int64_t n, double* tsdf,
+                     double* weight, double* s2, float* color) {
+  NEED(t);
+  return evict_blocks(T_(t), level, coords, n, tsdf, weight, s2, color);
+}
+
+int tsdf_import_level(tsdf_table* t, int32_t level, const int64_t* coords, int64_t n,
+                      const double* tsdf, const double* weight, const double* s2,
+                      const float* color) {
+  NEED(t);
+  return import_blocks(T_(t), level, coords, n, tsdf, weight, s2, color);
+}
+
 int tsdf_integrate_points(tsdf_table* t, const void* xyz, int32_t xyz_dtype, const void* rgb,
                           int32_t rgb_dtype, int64_t n, int32_t mem, const double* R,
                           const double* trans, double tau, double weight_cap,

@@ -129,6 +129,9 @@ int integrate_depth_walk(Table* T, const DepthArgs& a, int ray_rank, int ray_wor
                          uint64_t* buckets, uint64_t bucket_cap, int64_t* counts,
                          IntegrationStats* st);
 int integrate_depth_keys(Table* T, const uint64_t* keys, int64_t n, IntegrationStats* st);
+int depth_keys(Table* T, const DepthArgs& a, uint64_t* keys, int64_t cap, int64_t* n_out);
+int scan_keys(Table* T, const void* xyz, int xyz_dtype, int64_t n, int mem, const Frame& fr,
+              uint64_t* keys, int64_t cap, int64_t* n_out);
 int integrate_depth(Table* T, const void* depth, int depth_dtype, const void* rgb,
                     int rgb_dtype, int H, int W, int mem, const Frame& f,
                     IntegrationStats* st);
@@ -150,6 +153,10 @@ int read_block(Table* T, const int64_t* coord, int32_t* level, double* tsdf, dou
 int write_block(Table* T, const int64_t* coord, const double* tsdf, const double* weight,
                 const double* s2, const float* color);
 int live_count(Table* T, int32_t level, int64_t* n);
+int evict_blocks(Table* T, int32_t level, const int64_t* coords, int64_t n, double* tsdf,
+                 double* weight, double* s2, float* color);
+int import_blocks(Table* T, int32_t level, const int64_t* coords, int64_t n, const double* tsdf,
+                  const double* weight, const double* s2, const float* color);
 int export_level(Table* T, int32_t level, int64_t max_blocks, int64_t* coords, int64_t* handles,
                  double* tsdf, double* weight, double* s2, float* color, int64_t* n_out);
 

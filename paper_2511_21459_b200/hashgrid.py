@@ -293,8 +293,49 @@ class HashTable:
         return coords, handles, t, w, s2, col
 
     def live_blocks(self, level: int, sort: bool = True):
-        coords, handles, *_ = self.export_level(level)
+        """(coords, handles) of a level's live blocks in canonical (x, y, z)
+        order (hashgrid.py:345-354); no voxel payloads are moved."""
+        n = C.c_int64()
+        N.check(N.lib().tsdf_export_level(self._h, int(level), 0, None, None, None, None, None,
+                                          None, C.byref(n)), "live_blocks")
+        nb = int(n.value)
+        coords = np.zeros((nb, 3), dtype=np.int64)
+        handles = np.zeros(nb, dtype=np.int64)
+        if nb:
+            N.check(N.lib().tsdf_export_level(self._h, int(level), nb, coords.ctypes.data,
+                                              handles.ctypes.data, None, None, None, None,
+                                              C.byref(n)), "live_blocks")
         return coords, handles
+
+    # -- capacity tier: bulk block transfer ----------------------------------
+    def evict(self, level: int, coords):
+        """Remove live blocks of one level and return their payloads
+        (tsdf, weight, s2 f64 [n, nvox]; color f32 [n, nvox, 3]).  All or
+        nothing: NotFoundError if any block is not live at that level."""
+        c = np.ascontiguousarray(np.asarray(coords, dtype=np.int64).reshape(-1, 3))
+        n, nvox = len(c), self.heaps[level].nvox
+        t, w, s2 = (np.zeros((n, nvox)) for _ in range(3))
+        col = np.zeros((n, nvox, 3), dtype=np.float32)
+        if n:
+            N.check(N.lib().tsdf_evict_level(self._h, int(level), c, n, t.ctypes.data,
+                                             w.ctypes.data, s2.ctypes.data, col.ctypes.data),
+                    "evict")
+        return t, w, s2, col
+
+    def import_blocks(self, level: int, coords, tsdf, weight, s2, color) -> None:
+        """Insert blocks at `level` with their payloads (the inverse of
+        evict).  All or nothing: ValueError if one is already live,
+        CapacityError on heap / bucket-chain exhaustion."""
+        c = np.ascontiguousarray(np.asarray(coords, dtype=np.int64).reshape(-1, 3))
+        n, nvox = len(c), self.heaps[level].nvox
+        if n == 0:
+            return
+        t = np.ascontiguousarray(np.asarray(tsdf, dtype=np.float64).reshape(n, nvox))
+        w = np.ascontiguousarray(np.asarray(weight, dtype=np.float64).reshape(n, nvox))
+        s = np.ascontiguousarray(np.asarray(s2, dtype=np.float64).reshape(n, nvox))
+        col = np.ascontiguousarray(np.asarray(color, dtype=np.float32).reshape(n, nvox, 3))
+        N.check(N.lib().tsdf_import_level(self._h, int(level), c, n, t.ctypes.data, w.ctypes.data,
+                                          s.ctypes.data, col.ctypes.data), "import_blocks")
 
     def key_levels(self) -> dict:
         """{coord: level} of every live block (the parity key set)."""

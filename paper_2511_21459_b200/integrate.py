@@ -71,9 +71,39 @@ def update_voxel(v: Voxel, d_k: float, rgb=None, weight_cap: float = 0.0) -> Vox
     return Voxel(tsdf=mean, weight=w1, color=color, s2=s2)
 
 
-def _check_archive(archive):
-    if archive is not None and len(archive) != 0:
-        raise NotImplementedError("the streaming / archive tier is outside this build's scope")
+def _has_archive(archive) -> bool:
+    return archive is not None and len(archive) != 0
+
+
+def _stream_in_for(table: HashTable, frame, tau: float, archive) -> None:
+    """The archive branch of _ensure_blocks (integrate.py:122-140): archived
+    blocks the frame reaches come back, payload intact, before it is fused."""
+    if not _has_archive(archive):
+        return
+    from .streaming import stream_in_keys
+    keys = _frame_keys_tau(table, frame, tau)
+    stream_in_keys(table, archive, keys)
+
+
+def _frame_keys_tau(table: HashTable, frame, tau: float) -> np.ndarray:
+    """Distinct packed block keys the frame's allocation will touch (the
+    reference's np.unique of the DDA rows, integrate.py:203, :289), from a
+    key-only pass of the device DDA; the table is not changed."""
+    cap = max(1024, 2 * table.slots)
+    out = np.zeros(cap, dtype=np.uint64)
+    n = C.c_int64()
+    R, t = _pose(frame.pose)
+    if isinstance(frame, DepthFrame):
+        dptr, ddt, dmem, _keep = N.as_buffer(frame.depth, (N.F64, N.F32))
+        rc = N.lib().tsdf_depth_keys(table._h, dptr, ddt, frame.height, frame.width, dmem,
+                                     frame.intrinsics.as_array(), R, t, float(tau),
+                                     out.ctypes.data, cap, C.byref(n))
+    else:
+        pptr, pdt, pmem, _keep = N.as_buffer(frame.points, (N.F64, N.F32))
+        rc = N.lib().tsdf_scan_keys(table._h, pptr, pdt, int(frame.points.shape[0]), pmem, R, t,
+                                    float(tau), out.ctypes.data, cap, C.byref(n))
+    N.check(rc, "frame_keys")
+    return out[:n.value]
 
 
 def _stats(st) -> IntegrationStats:
@@ -91,10 +121,12 @@ def _pose(pose):
 
 def integrate_depth(table: HashTable, frame: DepthFrame, tau: float, archive=None,
                     weight_cap: float = 0.0) -> IntegrationStats:
-    """Projective fusion of one depth image (integrate.py:255-342)."""
+    """Projective fusion of one depth image (integrate.py:255-342).  With a
+    non-empty `archive` (streaming.ArchiveStore), archived blocks the frame
+    reaches are streamed back in first."""
     if tau <= 0:
         raise ValueError("tau must be positive")
-    _check_archive(archive)
+    _stream_in_for(table, frame, tau, archive)
     dptr, ddt, dmem, _keep_d = N.as_buffer(frame.depth, (N.F64, N.F32))
     cptr, cdt, cmem, _keep_c = (None, 0, dmem, None)
     if frame.color is not None:
@@ -172,11 +204,13 @@ def integrate_depth_batch(table: HashTable, frames, tau: float, archive=None,
     """
     if tau <= 0:
         raise ValueError("tau must be positive")
-    _check_archive(archive)
     frames = list(frames)
     n = len(frames)
     if n == 0:
         return []
+    if _has_archive(archive):
+        # stream-in depends on the table after the previous frame: per frame
+        return [integrate_depth(table, f, tau, archive, weight_cap) for f in frames]
     keep, dptrs, cptrs = [], [], []
     ddt = cdt = mem = None
     for f in frames:
@@ -213,13 +247,14 @@ def integrate_depth_batch(table: HashTable, frames, tau: float, archive=None,
 
 def integrate_pointcloud(table: HashTable, frame: PointCloudFrame, tau: float, archive=None,
                          weight_cap: float = 0.0) -> IntegrationStats:
-    """Ray-based fusion of one point cloud (integrate.py:175-252)."""
+    """Ray-based fusion of one point cloud (integrate.py:175-252); archived
+    blocks the scan reaches are streamed back in first."""
     if tau <= 0:
         raise ValueError("tau must be positive")
-    _check_archive(archive)
     n = int(frame.points.shape[0])
     if n == 0:
         return IntegrationStats()
+    _stream_in_for(table, frame, tau, archive)
     pptr, pdt, pmem, _keep_p = N.as_buffer(frame.points, (N.F64, N.F32))
     cptr, cdt, _keep_c = None, 0, None
     if frame.colors is not None:
@@ -239,9 +274,18 @@ def allocate_for_measurement(table: HashTable, origin, p, tau: float, archive=No
     (integrate.py:143-161); handles in traversal order."""
     if tau <= 0:
         raise ValueError("tau must be positive")
-    _check_archive(archive)
     o = np.ascontiguousarray(origin, dtype=np.float64).reshape(3)
     q = np.ascontiguousarray(p, dtype=np.float64).reshape(3)
+    if _has_archive(archive):
+        from .dda import dda_blocks
+        from .streaming import _pack, stream_in_keys
+        ray = q - o
+        n_ = np.linalg.norm(ray)
+        if n_ == 0.0:
+            raise ValueError("measurement coincides with the sensor origin")
+        end = q + tau * ray / n_  # integrate.py:157, same evaluation order
+        coords = np.asarray(dda_blocks(o, end, table.block_edge), dtype=np.int64).reshape(-1, 3)
+        stream_in_keys(table, archive, np.unique(_pack(coords)))
     cap = 1 << 16
     out = np.zeros(cap, dtype=np.int64)
     n = C.c_int64()
