@@ -177,6 +177,19 @@ def window(P, t, wl, frs, dev=None):
     return [integrate(P, t, wl, fr, None if dev is None else dev[i]) for i, fr in enumerate(frs)]
 
 
+def window_and_merge(P, t, wl, frs, dev=None):
+    """One step: a merge window plus its merge pass.  Single-GPU depth
+    windows go through integrate_depth_window (frames + merge pass enqueued
+    together, one host synchronisation); otherwise window() + apply_merges."""
+    if wl["kind"] == "depth" and not _MULTI:
+        fs = [P.DepthFrame(depth=fr[0] if dev is None else dev[i][0], intrinsics=fr[3], pose=fr[2],
+                           color=fr[1] if dev is None else dev[i][1]) for i, fr in enumerate(frs)]
+        stats, ms = P.integrate_depth_window(t, fs, wl["tau"], wl["sigma"], all_levels=True)
+        return stats, ms.merged
+    stats = window(P, t, wl, frs, dev)
+    return stats, P.apply_merges(t, wl["sigma"], all_levels=True).merged
+
+
 def kernel_bytes(stats_list, wl):
     """Algorithmic bytes: B = s_in*P + 16*T + 16*A + 48*U per frame."""
     s_in = S_IN[wl["kind"]]
@@ -224,9 +237,9 @@ def run_b200(args, wl, rank, world, dist, torch):
     all_stats, step_ms, merged = [], [], 0
     fi = 0
     for s in range(W):
-        window(P, table, wl, frames[fi:fi + FRAMES_PER_STEP], dframes[fi:fi + FRAMES_PER_STEP])
+        window_and_merge(P, table, wl, frames[fi:fi + FRAMES_PER_STEP],
+                         dframes[fi:fi + FRAMES_PER_STEP])
         fi += FRAMES_PER_STEP
-        P.apply_merges(table, wl["sigma"], all_levels=True)
     launches0 = table.kernel_launches
     barrier()
     sampler = ClockSampler(dev.index)
@@ -237,10 +250,11 @@ def run_b200(args, wl, rank, world, dist, torch):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            all_stats += window(P, table, wl, frames[fi:fi + FRAMES_PER_STEP],
-                                dframes[fi:fi + FRAMES_PER_STEP])
+            st_, m_ = window_and_merge(P, table, wl, frames[fi:fi + FRAMES_PER_STEP],
+                                       dframes[fi:fi + FRAMES_PER_STEP])
+            all_stats += st_
+            merged += m_
             fi += FRAMES_PER_STEP
-            merged += P.apply_merges(table, wl["sigma"], all_levels=True).merged
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -255,10 +269,9 @@ def run_b200(args, wl, rank, world, dist, torch):
     for s in range(K):
         flush.fill_(s & 0xFF)
         torch.cuda.synchronize()
-        prof_stats += window(P, table, wl, frames[fi:fi + FRAMES_PER_STEP],
-                             dframes[fi:fi + FRAMES_PER_STEP])
+        prof_stats += window_and_merge(P, table, wl, frames[fi:fi + FRAMES_PER_STEP],
+                                       dframes[fi:fi + FRAMES_PER_STEP])[0]
         fi += FRAMES_PER_STEP
-        P.apply_merges(table, wl["sigma"], all_levels=True)
     torch.cuda.synchronize()
     ktimes = table.kernel_times(reset=True)
     work = table.work_totals(reset=True)
@@ -288,21 +301,19 @@ def run_b200(args, wl, rank, world, dist, torch):
     fi = 0
     pinned = pinned[:FRAMES_PER_STEP * (W + K)]
     for s in range(W):
-        window(P, t2, wl, pinned[fi:fi + FRAMES_PER_STEP])
+        window_and_merge(P, t2, wl, pinned[fi:fi + FRAMES_PER_STEP])
         fi += FRAMES_PER_STEP
-        P.apply_merges(t2, wl["sigma"], all_levels=True)
     barrier()
     e2e_t0 = time.perf_counter()
     e2e_pts = 0
     for s in range(K):
         win = pinned[fi:fi + FRAMES_PER_STEP]
-        sts = window(P, t2, wl, win)
+        sts, _ = window_and_merge(P, t2, wl, win)
         e2e_pts += sum(st.measurements for st in sts)
         for fr in win:
             h2d += fr[0].nbytes + (0 if fr[1] is None else fr[1].nbytes)
             d2h += 192  # per-frame counters block (stats) read back
         fi += FRAMES_PER_STEP
-        P.apply_merges(t2, wl["sigma"], all_levels=True)
         d2h += 192
     barrier()
     e2e_s = time.perf_counter() - e2e_t0

@@ -392,6 +392,46 @@ int tsdf_integrate_depth_batch(tsdf_table* t, int32_t n_frames, const void* cons
   return s;
 }
 
+int tsdf_integrate_depth_window(tsdf_table* t, int32_t n_frames, const void* const* depth,
+                               int32_t depth_dtype, const void* const* rgb, int32_t rgb_dtype,
+                               int32_t height, int32_t width, int32_t mem, const double* K,
+                               const double* R, const double* trans, double tau,
+                               double weight_cap, tsdf_integration_stats* stats,
+                               int32_t* n_done, double sigma, double min_frac, double min_w,
+                               int32_t all_levels, tsdf_merge_stats* merge_stats) {
+  NEED(t);
+  if (n_frames <= 0) {
+    *n_done = 0;
+    return TSDF_OK;
+  }
+  if (depth_dtype < 0 || depth_dtype > 3 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  std::vector<DepthArgs> args(n_frames);
+  for (int i = 0; i < n_frames; i++) {
+    if (K[4 * i] <= 0 || K[4 * i + 1] <= 0) {
+      set_error("focal lengths must be positive");
+      return TSDF_EDATASET;
+    }
+    args[i] = DepthArgs{depth[i], depth_dtype, rgb ? rgb[i] : nullptr, rgb_dtype, height, width,
+                        mem, make_frame(K + 4 * i, R + 9 * i, trans + 3 * i, tau, weight_cap)};
+  }
+  std::vector<IntegrationStats> st(n_frames);
+  int done = 0;
+  MergeArgs ma{sigma, min_frac, min_w, all_levels};
+  MergeStats ms{0, 0};
+  int s = integrate_depth_window(T_(t), n_frames, args.data(), st.data(), &done,
+                                 merge_stats ? &ma : nullptr, &ms);
+  if (merge_stats) {
+    merge_stats->candidates = ms.candidates;
+    merge_stats->merged = ms.merged;
+  }
+  for (int i = 0; i < n_frames; i++) memcpy(&stats[i], &st[i], sizeof(st[i]));
+  *n_done = done;
+  return s;
+}
+
 }  // extern "C"
 
 extern "C" int tsdf_work_totals(tsdf_table* t, int64_t* out, int32_t reset) {

@@ -49,6 +49,7 @@ struct Table {
   Buf cand_l[kMaxLevels];
   Buf batch, pyr, lidar_aux;
   Buf dblk, dmicro, dexact;  // depth update work lists (blocks, micro-bricks, voxels)
+  Buf mdev;                  // MergeDev of the last enqueued merge pass
   // depth batches overlap frame k+1's allocation (walk stream) with frame
   // k's voxel update (main stream): per-parity copies of the frame scratch
   // that both sides read
@@ -125,6 +126,12 @@ struct DepthArgs {
 };
 int integrate_depth_batch(Table* T, int B, const DepthArgs* frames, IntegrationStats* st,
                           int* n_done);
+struct MergeArgs {
+  double sigma, min_frac, min_w;
+  int all_levels;
+};
+int integrate_depth_window(Table* T, int B, const DepthArgs* frames, IntegrationStats* st,
+                           int* n_done, const MergeArgs* merge, MergeStats* mst);
 int integrate_depth_walk(Table* T, const DepthArgs& a, int ray_rank, int ray_world,
                          uint64_t* buckets, uint64_t bucket_cap, int64_t* counts,
                          IntegrationStats* st);

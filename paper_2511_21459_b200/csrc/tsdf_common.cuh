@@ -116,6 +116,15 @@ struct Counters {
   uint32_t free_top[kMaxLevels];
 };
 
+// device counters of one merge pass (enqueue_merges)
+struct MergeDev {
+  unsigned long long n_cand[kMaxLevels];
+  unsigned long long n_list;
+  unsigned long long n_dirty;  // dirty-list length at the pass (snapshot)
+  uint32_t skip;
+  uint32_t pad;
+};
+
 __host__ __device__ inline uint64_t pack_key(int64_t x, int64_t y, int64_t z) {
   return ((uint64_t)(x + kCoordBias) << 42) | ((uint64_t)(y + kCoordBias) << 21) |
          (uint64_t)(z + kCoordBias);

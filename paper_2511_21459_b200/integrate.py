@@ -195,22 +195,44 @@ def integrate_depth_keys(table: HashTable, keys, n: int = None) -> IntegrationSt
 
 def integrate_depth_batch(table: HashTable, frames, tau: float, archive=None,
                           weight_cap: float = 0.0) -> list:
-    """Integrate the frames of one merge window with a single host sync.
-
-    Same result as calling ``integrate_depth`` on each frame in order (the
-    table only changes at merge boundaries outside this call); on an error
-    at frame i the later frames are not applied and the error is raised.
-    All frames must share size and dtypes.
-    """
+    """Fuse a merge window of depth frames with one host synchronisation
+    (the same results as integrate_depth per frame).  On an error at frame i
+    the later frames are not applied and the error is raised.  All frames
+    must share size and dtypes."""
     if tau <= 0:
         raise ValueError("tau must be positive")
     frames = list(frames)
-    n = len(frames)
-    if n == 0:
+    if not frames:
         return []
     if _has_archive(archive):
         # stream-in depends on the table after the previous frame: per frame
         return [integrate_depth(table, f, tau, archive, weight_cap) for f in frames]
+    return _depth_window(table, frames, tau, weight_cap, None)[0]
+
+
+def integrate_depth_window(table: HashTable, frames, tau: float, sigma_threshold: float,
+                           min_eligible_fraction: float = 0.05, min_mean_weight: float = 3.0,
+                           all_levels: bool = False, weight_cap: float = 0.0):
+    """One merge window of the reference's engine loop (pipeline.py:88-137):
+    the frames, then one apply_merges pass, enqueued back to back on the
+    device with a single host synchronisation.  Returns (per-frame stats,
+    MergeStats).  If a frame fails, the later frames and the merge are not
+    applied and the error is raised."""
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    if not sigma_threshold > 0:
+        raise ValueError("sigma_threshold must be positive")
+    frames = list(frames)
+    if not frames:
+        from .adapt import apply_merges
+        return [], apply_merges(table, sigma_threshold, min_eligible_fraction, min_mean_weight,
+                                all_levels=all_levels)
+    return _depth_window(table, frames, tau, weight_cap,
+                         (sigma_threshold, min_eligible_fraction, min_mean_weight, all_levels))
+
+
+def _depth_window(table, frames, tau, weight_cap, merge):
+    n = len(frames)
     keep, dptrs, cptrs = [], [], []
     ddt = cdt = mem = None
     for f in frames:
@@ -238,11 +260,18 @@ def integrate_depth_batch(table: HashTable, frames, tau: float, archive=None,
     carr = (C.c_void_p * n)(*cptrs) if cptrs else None
     st = (N.IntegrationStatsC * n)()
     done = C.c_int32()
-    rc = N.lib().tsdf_integrate_depth_batch(table._h, n, darr, ddt, carr, cdt or 0,
-                                            frames[0].height, frames[0].width, mem, K, R, T,
-                                            float(tau), float(weight_cap), st, C.byref(done))
-    N.check(rc, "integrate_depth_batch")
-    return [_stats(s) for s in st]
+    ms = N.MergeStatsC()
+    sig, frac, minw, alll = merge if merge is not None else (0.0, 0.0, 0.0, False)
+    rc = N.lib().tsdf_integrate_depth_window(table._h, n, darr, ddt, carr, cdt or 0,
+                                             frames[0].height, frames[0].width, mem, K, R, T,
+                                             float(tau), float(weight_cap), st, C.byref(done),
+                                             float(sig), float(frac), float(minw), int(bool(alll)),
+                                             C.byref(ms) if merge is not None else None)
+    N.check(rc, "integrate_depth_batch" if merge is None else "integrate_depth_window")
+    from .adapt import MergeStats
+    return [_stats(s) for s in st], MergeStats(int(ms.candidates), int(ms.merged))
+
+
 
 
 def integrate_pointcloud(table: HashTable, frame: PointCloudFrame, tau: float, archive=None,

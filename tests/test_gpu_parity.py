@@ -420,6 +420,41 @@ def test_ray_sharded_keys_need_walk_and_routing():
         P.integrate_depth_keys(t, torch.as_tensor(foreign, device=dev))
 
 
+@pytest.mark.parametrize("all_levels", [False, True])
+def test_depth_window_equals_batch_then_merge(all_levels):
+    """integrate_depth_window (frames + merge pass, one host sync) ==
+    integrate_depth_batch followed by apply_merges, window after window."""
+    import paper_2511_21459_b200 as P
+    frames = P.synth.render_frames("room", 30, 160, 120, depth_dtype=np.float32,
+                                   color_dtype=np.uint8)
+    caps = (100000, 20000, 5000)
+    a = P.HashTable(1000003, 10, 7, 0.04, caps)
+    b = P.HashTable(1000003, 10, 7, 0.04, caps)
+    for w in range(3):
+        win = frames[10 * w:10 * (w + 1)]
+        sa, ma = P.integrate_depth_window(a, win, 0.015, 2.5e-5, all_levels=all_levels)
+        sb = P.integrate_depth_batch(b, win, 0.015)
+        mb = P.apply_merges(b, 2.5e-5, all_levels=all_levels)
+        assert [vars(x) for x in sa] == [vars(x) for x in sb]
+        assert (ma.candidates, ma.merged) == (mb.candidates, mb.merged)
+    assert PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": a})())) == \
+        PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": b})()))
+
+
+def test_merge_heap_exhaustion_changes_nothing():
+    """A merge pass whose candidates do not fit the coarse heap raises
+    CapacityError and moves nothing (adapt.py / the device check)."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200.errors import CapacityError
+    b, _, _, _ = PU.run_depth_scenario("gpu", "sphere", 20, 48, 36, 0.08, 0.03, (20000, 3), 100003)
+    t = b.t
+    before = PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": t})()))
+    assert len(P.select_merge_candidates(t, 2.5e-4)) > 3
+    with pytest.raises(CapacityError):
+        P.apply_merges(t, 2.5e-4)
+    assert PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": t})())) == before
+
+
 def test_depth_batch_equals_per_frame_and_oracle():
     """integrate_depth_batch (one host sync per merge window) == per-frame calls == oracle."""
     import paper_2511_21459_b200 as P
