@@ -41,12 +41,29 @@ WORKLOADS = {
                  cadence=10, frames_total=500,
                  name="large room 6x5x3 m, 640x480 RGB-D (f32 depth + u8 RGB), 3 levels 5/10/20 mm, "
                       "500-frame sweep, merge every 10 frames"),
+    # BASELINE config 4: fixed 5 mm, single level (no merges), large hash
+    # table and a ~100 GB level-0 heap (the hash-capacity / memory stress)
+    "room_fixed5mm": dict(kind="depth", scene="large_room", width=640, height=480, edge=0.04,
+                          tau=0.015, sigma=5e-324, caps=(6_000_000,), n_hash=16_000_057,
+                          cadence=10, frames_total=500,
+                          name="large room 6x5x3 m, 640x480 RGB-D, fixed 5 mm single level "
+                               "(merges off), 6M-block (98 GB) heap, 16M-slot hash"),
+    # BASELINE config 5 (depth part): 1024x768 frames of the large room
+    "room1024": dict(kind="depth", scene="large_room", width=1024, height=768, edge=0.04,
+                     tau=0.015, sigma=2.5e-5, caps=(2_500_000, 500_000, 150_000),
+                     n_hash=8_000_009, cadence=10, frames_total=500,
+                     name="large room 6x5x3 m, 1024x768 RGB-D, 3 levels 5/10/20 mm, "
+                          "merge every 10 frames"),
     "lidar": dict(kind="lidar", beams=128, columns=2048, edge=1.6, tau=0.8, sigma=1e-2,
                   caps=(1_500_000, 200_000, 50_000), n_hash=4_000_037, cadence=10, step_m=0.5,
                   name="128-beam x 2048-column LiDAR, 100 m range, 0.2/0.4/0.8 m levels, "
                        "sensor advancing 0.5 m/scan, merge every 10 scans"),
 }
-FRAMES_PER_STEP = 10
+METRIC = {"room": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)",
+          "room_fixed5mm": "integrated Mpoints/s (640x480 RGB-D room, fixed 5 mm)",
+          "room1024": "integrated Mpoints/s (1024x768 RGB-D room, 3 levels)",
+          "lidar": "integrated Mpoints/s (128-beam LiDAR)"}
+FRAMES_PER_STEP = int(os.environ.get("TSDF_BENCH_WINDOW", "10"))  # = merge cadence
 S_IN = {"depth": 7, "lidar": 12}  # algorithmic input bytes per measurement
 
 
@@ -354,8 +371,7 @@ def run_b200(args, wl, rank, world, dist, torch):
                      "gsteps_per_s": round(steps / (w_ms / max(w_n, 1) * 1e-3) / 1e9, 3),
                      "ncu_issue_active_frac": ncu.get("issue_active_frac", {}).get("k_dda_walk")}
     out = {
-        "metric": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)" if wl["kind"] == "depth"
-                  else "integrated Mpoints/s (128-beam LiDAR)",
+        "metric": METRIC[args.workload],
         "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(dev_ms / K, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -392,7 +408,7 @@ def run_oracle_frames(wl, frames):
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle.oracle import OracleTable
     # heaps sized for the bounded sample (calloc'd pages are only committed on touch)
-    t = OracleTable(wl["n_hash"], 10, 7, wl["edge"], (600_000, 40_000, 10_000))
+    t = OracleTable(wl["n_hash"], 10, 7, wl["edge"], (600_000, 40_000, 10_000)[:len(wl["caps"])])
     pts, secs = 0, []
     for d, c, pose, intr in frames:
         t0 = time.perf_counter()
@@ -422,8 +438,7 @@ def run_reference(args, wl):
     tp = sum(secs[args.warmup:])
     ppts = sum(n_meas(f) for f in frames[args.warmup:])
     v = ppts / tp / 1e6
-    return {"impl": "reference", "metric": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)"
-            if wl["kind"] == "depth" else "integrated Mpoints/s (128-beam LiDAR)",
+    return {"impl": "reference", "metric": METRIC[args.workload],
             "value": round(v, 4), "unit": "Mpoints/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(tp / args.steps * 1e3, 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
