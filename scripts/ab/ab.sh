@@ -1,0 +1,8 @@
+# A/B: bench each fusion_*.cu variant on the same box (rebuilds in place)
+for v in ${VARIANTS:-A B}; do
+  cp scripts/ab/fusion_$v.cu paper_2511_21459_b200/csrc/fusion.cu
+  (cd paper_2511_21459_b200/csrc && make -s -j8 > /dev/null 2>&1)
+  for r in 1 2; do
+    python bench.py --no-cpu-baseline --steps 5 ${BENCH_ARGS} > gpurun_out/ab_${v}_$r.json 2>/dev/null
+  done
+done
