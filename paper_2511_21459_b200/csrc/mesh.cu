@@ -51,15 +51,30 @@ static int load_tables() {
 }
 
 // scratch buffers owned by one extraction call
+// per-call device scratch from the stream-ordered pool: after the first
+// extraction the pool keeps the memory, so later calls allocate for free
 struct DevBuf {
   std::vector<void*> ptrs;
+  cudaStream_t stream = nullptr;
+  static void keep_pool() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done = true;
+  }
   ~DevBuf() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
   }
   template <class T>
   T* get(size_t n) {
+    keep_pool();
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), stream) != cudaSuccess) return nullptr;
     ptrs.push_back(p);
     return (T*)p;
   }
@@ -633,15 +648,17 @@ struct Scratch {
   DevBuf bufs;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
+  explicit Scratch(cudaStream_t st = nullptr) { bufs.stream = st; }
   ~Scratch() {
-    if (tmp) cudaFree(tmp);
+    if (tmp) cudaFreeAsync(tmp, bufs.stream);
   }
   int need(size_t b) {
     if (b <= tmp_bytes) return kOk;
-    if (tmp) cudaFree(tmp);
+    if (tmp) cudaFreeAsync(tmp, bufs.stream);
     tmp = nullptr;
     tmp_bytes = 0;
-    if (cudaMalloc(&tmp, b) != cudaSuccess) {
+    DevBuf::keep_pool();
+    if (cudaMallocAsync(&tmp, b, bufs.stream) != cudaSuccess) {
       set_error("device allocation failed for sort scratch");
       return kCapacityError;
     }
@@ -781,7 +798,7 @@ int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
   MCK(cudaStreamSynchronize(st));
   const DevTable& d = T->d;
   uint64_t slots = T->slots;
-  Scratch S;
+  Scratch S(st);
   uint8_t* obs = S.bufs.get<uint8_t>(slots);
   double* rlo = S.bufs.get<double>(slots);
   double* rhi = S.bufs.get<double>(slots);
