@@ -56,6 +56,8 @@ struct Table {
   // that both sides read
   Buf in0b, in1b, drayb, flagsb, pyrb, touchedb;
   cudaStream_t walk_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // H2D of host frames, ahead of the walk stream
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_start = nullptr, ev_alloc[2] = {nullptr, nullptr}, ev_upd[2] = {nullptr, nullptr};
   cudaStream_t prof_stream = nullptr;  // stream the profiling events go to (null: stream)
   // ray-sharded allocation (multi-GPU): per-frame "emitted" key set and the
