@@ -135,14 +135,19 @@ int tsdf_integrate_depth_batch(tsdf_table *t, int32_t n_frames, const void *cons
  * frames followed -- when merge_stats is not NULL and every frame
  * succeeded -- by one tsdf_apply_merges pass (sigma, min_frac, min_w,
  * all_levels), all enqueued back to back with a single host
- * synchronisation. */
+ * synchronisation (sigma <= 0: no merge pass).  fill_limit > 0 (with
+ * merge_stats): the window stops
+ * after the first frame i < n_frames - 1 that brings a level's occupancy
+ * to fill_limit (the engine's stream-out mark); *n_done = i + 1, the
+ * merge is not run and TSDF_OK is returned. */
 int tsdf_integrate_depth_window(tsdf_table *t, int32_t n_frames, const void *const *depth,
                                 int32_t depth_dtype, const void *const *rgb, int32_t rgb_dtype,
                                 int32_t height, int32_t width, int32_t mem, const double *K,
                                 const double *R, const double *trans, double tau,
                                 double weight_cap, tsdf_integration_stats *stats,
                                 int32_t *n_done, double sigma, double min_frac, double min_w,
-                                int32_t all_levels, tsdf_merge_stats *merge_stats);
+                                int32_t all_levels, double fill_limit,
+                                tsdf_merge_stats *merge_stats);
 
 /* integrate_pointcloud(table, PointCloudFrame, tau, weight_cap) --
  * integrate.py:175-252.  xyz: n*3 sensor-frame points; rgb n*3 or NULL. */

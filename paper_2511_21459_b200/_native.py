@@ -80,7 +80,7 @@ def lib():
     L.tsdf_integrate_depth_window.argtypes = [_ptr, i32, _ptr, i32, _ptr, i32, i32, i32, i32,
                                               _f64p, _f64p, _f64p, dbl, dbl,
                                               C.POINTER(IntegrationStatsC), C.POINTER(i32), dbl,
-                                              dbl, dbl, i32, C.POINTER(MergeStatsC)]
+                                              dbl, dbl, i32, dbl, C.POINTER(MergeStatsC)]
     L.tsdf_integrate_depth_walk.argtypes = [_ptr, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p,
                                             _f64p, _f64p, dbl, dbl, i32, i32, _ptr, i64, _i64p,
                                             C.POINTER(IntegrationStatsC)]

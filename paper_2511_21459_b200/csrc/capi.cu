@@ -398,7 +398,8 @@ int tsdf_integrate_depth_window(tsdf_table* t, int32_t n_frames, const void* con
                                const double* R, const double* trans, double tau,
                                double weight_cap, tsdf_integration_stats* stats,
                                int32_t* n_done, double sigma, double min_frac, double min_w,
-                               int32_t all_levels, tsdf_merge_stats* merge_stats) {
+                               int32_t all_levels, double fill_limit,
+                               tsdf_merge_stats* merge_stats) {
   NEED(t);
   if (n_frames <= 0) {
     *n_done = 0;
@@ -419,7 +420,7 @@ int tsdf_integrate_depth_window(tsdf_table* t, int32_t n_frames, const void* con
   }
   std::vector<IntegrationStats> st(n_frames);
   int done = 0;
-  MergeArgs ma{sigma, min_frac, min_w, all_levels};
+  MergeArgs ma{sigma, min_frac, min_w, all_levels, fill_limit};
   MergeStats ms{0, 0};
   int s = integrate_depth_window(T_(t), n_frames, args.data(), st.data(), &done,
                                  merge_stats ? &ma : nullptr, &ms);

@@ -132,6 +132,7 @@ int integrate_depth_batch(Table* T, int B, const DepthArgs* frames, IntegrationS
 struct MergeArgs {
   double sigma, min_frac, min_w;
   int all_levels;
+  double fill_limit;  // > 0: stop after the frame that brings a level to this occupancy
 };
 int integrate_depth_window(Table* T, int B, const DepthArgs* frames, IntegrationStats* st,
                            int* n_done, const MergeArgs* merge, MergeStats* mst);

@@ -227,11 +227,16 @@ def integrate_depth_window(table: HashTable, frames, tau: float, sigma_threshold
         from .adapt import apply_merges
         return [], apply_merges(table, sigma_threshold, min_eligible_fraction, min_mean_weight,
                                 all_levels=all_levels)
-    return _depth_window(table, frames, tau, weight_cap,
-                         (sigma_threshold, min_eligible_fraction, min_mean_weight, all_levels))
+    st, ms, _ = _depth_window(table, frames, tau, weight_cap,
+                              (sigma_threshold, min_eligible_fraction, min_mean_weight, all_levels))
+    return st, ms
 
 
-def _depth_window(table, frames, tau, weight_cap, merge):
+def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial=False):
+    """-> (stats of the frames applied, MergeStats, frames applied); with
+    partial=True a failing frame does not raise: its error is returned as a
+    fourth element (None if every frame was applied or the fill mark stopped
+    the window)."""
     n = len(frames)
     keep, dptrs, cptrs = [], [], []
     ddt = cdt = mem = None
@@ -266,10 +271,19 @@ def _depth_window(table, frames, tau, weight_cap, merge):
                                              frames[0].height, frames[0].width, mem, K, R, T,
                                              float(tau), float(weight_cap), st, C.byref(done),
                                              float(sig), float(frac), float(minw), int(bool(alll)),
+                                             float(fill_limit),
                                              C.byref(ms) if merge is not None else None)
-    N.check(rc, "integrate_depth_batch" if merge is None else "integrate_depth_window")
     from .adapt import MergeStats
-    return [_stats(s) for s in st], MergeStats(int(ms.candidates), int(ms.merged))
+    k = int(done.value)
+    if rc and partial:
+        # frames before the failing one are applied: report them with the error
+        try:
+            N.check(rc, "integrate_depth_window")
+        except Exception as exc:
+            return [_stats(s) for s in st[:k]], MergeStats(), k, exc
+    N.check(rc, "integrate_depth_batch" if merge is None else "integrate_depth_window")
+    out = [_stats(s) for s in st[:k]], MergeStats(int(ms.candidates), int(ms.merged)), k
+    return out + (None,) if partial else out
 
 
 

@@ -102,6 +102,8 @@ def main():
                         pose=SensorPose(f.pose.rotation, f.pose.translation),
                         color=None if f.color is None else PU._color_f64(f.color))
         st = eng.integrate_frame(rf)
+        eng.maybe_merge()
+        eng.maybe_stream()
         per.append({**{k: getattr(st, k) for k in PU.STAT_KEYS}, "archived": len(eng.archive),
                     "live": [h.occupied for h in eng.table.heaps]})
     gold["forced"] = {"per_frame": per, "state_digest": PU.state_digest(ref_state(eng.table)),

@@ -101,6 +101,8 @@ def test_capacity_error_evicts_and_retries():
     per = []
     for f in stream_frames()[:20]:
         st = eng.integrate_frame(f)
+        eng.maybe_merge()
+        eng.maybe_stream()
         per.append({**{k: getattr(st, k) for k in PU.STAT_KEYS}, "archived": len(eng.archive),
                     "live": [h.occupied for h in eng.table.heaps]})
     g = GOLD["forced"]
@@ -109,3 +111,35 @@ def test_capacity_error_evicts_and_retries():
     assert eng.evicted_blocks == g["evicted_blocks"] > 0
     assert PU.state_digest(_state(eng.table)) == g["state_digest"]
     assert not set(map(tuple, eng.table.key_levels())) & set(eng.archive.coords())
+
+
+@pytest.mark.parametrize("which", ["stream", "forced"])
+def test_engine_windows_match_reference(which):
+    """FusionEngine.integrate_frames (device windows up to each merge
+    boundary, stopping at the stream-out mark or a heap overflow) gives the
+    reference's per-frame results: stats, evictions, archive and state."""
+    import paper_2511_21459_b200 as P
+    cfg = P.PipelineConfig(**STREAM_SPEC["config"]) if which == "stream" else \
+        P.PipelineConfig(**{**STREAM_SPEC["config"], **FORCED})
+    frames = stream_frames() if which == "stream" else stream_frames()[:20]
+    eng = P.FusionEngine(cfg)
+    st = eng.integrate_frames(frames)
+    g = GOLD[which]
+    assert [{k: getattr(s, k) for k in PU.STAT_KEYS} for s in st] == \
+        [{k: r[k] for k in PU.STAT_KEYS} for r in g["per_frame"]]
+    assert eng.evicted_blocks == g["evicted_blocks"]
+    assert PU.state_digest(_state(eng.table)) == g["state_digest"]
+    if which == "stream":
+        assert [list(c) for c in eng.archive.coords()] == g["archive_coords"]
+
+
+def test_run_pipeline_batched_equals_per_frame():
+    import paper_2511_21459_b200 as P
+    frames = P.synth.render_frames("room", 25, 64, 48, depth_dtype=np.float32, color_dtype=np.uint8)
+    cfg = P.PipelineConfig(sensor_mode="depth", nu_fine=0.01, block_edge=0.08, tau=0.04,
+                           n_hash=100003, heap_capacity_fine=20000, heap_capacity_coarse=10000)
+    ra, ma = P.run_pipeline(cfg, frames, batched=True)
+    rb, mb = P.run_pipeline(cfg, frames, batched=False)
+    assert ra.frames == rb.frames == 25 and ra.merged_blocks == rb.merged_blocks > 0
+    assert ra.live_blocks == rb.live_blocks
+    assert np.array_equal(ma.vertices, mb.vertices) and np.array_equal(ma.triangles, mb.triangles)
