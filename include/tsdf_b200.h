@@ -38,7 +38,7 @@ extern "C" {
 #define TSDF_F64 0
 #define TSDF_F32 1
 #define TSDF_U8 2  /* colour channels: value/255.0, as datasets.py:118,163 */
-#define TSDF_U16 3
+#define TSDF_U16 3 /* depth: raw units / depth_scale (tsdf_table_set_depth_scale) */
 
 #define TSDF_MEM_HOST 0
 #define TSDF_MEM_DEVICE 1
@@ -86,6 +86,11 @@ int tsdf_table_reset(tsdf_table *t);
 /* block-key-hash sharding: this table owns only keys with
  * owner(key) == rank (world > 1); DESIGN.md "Multi-GPU". */
 int tsdf_table_set_shard(tsdf_table *t, int32_t rank, int32_t world);
+/* Units of raw uint16 depth (depth_dtype 3) for the following depth calls:
+ * z = raw / depth_scale in f64, the conversion the reference's reader does
+ * on the host (datasets.py:108-113, config.py:42 default 5000); default 1.0.
+ * Lets a dataset's 16-bit PNG depth cross PCIe at 2 B/px. */
+int tsdf_table_set_depth_scale(tsdf_table *t, double depth_scale);
 
 /* integrate_depth(table, DepthFrame, tau, weight_cap) -- integrate.py:255-342.
  * depth: H*W z-depth in metres (0 / NaN invalid); rgb: H*W*3 or NULL.
@@ -172,6 +177,15 @@ int tsdf_apply_merges(tsdf_table *t, double sigma_threshold, double min_eligible
  * collapse_epsilon < 0 selects the default 0.25 * voxel_size(0). */
 int tsdf_extract_mesh(tsdf_table *t, double iso, double collapse_epsilon, tsdf_mesh *out);
 void tsdf_mesh_free(tsdf_mesh *m);
+
+/* Nearest-neighbour distance from every query point to the tree point set
+ * (FP64, sqrt((dx*dx + dy*dy) + dz*dz), exact): the cKDTree(tree).query(q,
+ * k=1)[0] of eval_reconstruction (metrics.py:63-64).  Points are n x 3 f64;
+ * mem says where tree, query and dist live (TSDF_MEM_HOST / _DEVICE).  A
+ * non-finite query gets NaN; a non-finite tree point is TSDF_EVALUE.
+ * Table-independent; runs on cuda_stream (NULL: legacy default stream). */
+int tsdf_nn_distance(const double *tree, int64_t n_tree, const double *query, int64_t n_query,
+                     int32_t mem, double *dist, void *cuda_stream);
 
 /* HashTable.find_batch (hashgrid.py:300-331) */
 int tsdf_find_batch(tsdf_table *t, const int64_t *coords, int64_t n, int64_t *handles,

@@ -72,6 +72,7 @@ def lib():
     L.tsdf_table_destroy.argtypes = [_ptr]
     L.tsdf_table_reset.argtypes = [_ptr]
     L.tsdf_table_set_shard.argtypes = [_ptr, i32, i32]
+    L.tsdf_table_set_depth_scale.argtypes = [_ptr, C.c_double]
     L.tsdf_integrate_depth.argtypes = [_ptr, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p, _f64p,
                                        _f64p, dbl, dbl, C.POINTER(IntegrationStatsC)]
     L.tsdf_integrate_depth_batch.argtypes = [_ptr, i32, _ptr, i32, _ptr, i32, i32, i32, i32,
@@ -92,6 +93,7 @@ def lib():
     L.tsdf_apply_merges.argtypes = [_ptr, dbl, dbl, dbl, i32, C.POINTER(MergeStatsC)]
     L.tsdf_extract_mesh.argtypes = [_ptr, dbl, dbl, C.POINTER(MeshC)]
     L.tsdf_mesh_free.argtypes = [C.POINTER(MeshC)]
+    L.tsdf_nn_distance.argtypes = [_ptr, i64, _ptr, i64, i32, _ptr, _ptr]
     L.tsdf_find_batch.argtypes = [_ptr, _i64p, i64, _i64p, np.ctypeslib.ndpointer(np.int32),
                                   np.ctypeslib.ndpointer(np.uint8)]
     L.tsdf_insert.argtypes = [_ptr, _i64p, i32, C.POINTER(i64)]

@@ -1,4 +1,5 @@
 // extern "C" boundary (include/tsdf_b200.h) over the device implementation.
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -70,6 +71,16 @@ int tsdf_table_set_shard(tsdf_table* t, int32_t rank, int32_t world) {
   }
   T_(t)->d.shard_rank = rank;
   T_(t)->d.shard_world = world;
+  return TSDF_OK;
+}
+
+int tsdf_table_set_depth_scale(tsdf_table* t, double depth_scale) {
+  NEED(t);
+  if (!(depth_scale > 0.0) || !std::isfinite(depth_scale)) {
+    set_error("depth_scale must be positive and finite");
+    return TSDF_EVALUE;
+  }
+  T_(t)->depth_scale = depth_scale;
   return TSDF_OK;
 }
 

@@ -43,6 +43,7 @@ struct Table {
   Counters* dcnt = nullptr;  // device
   Counters* hcnt = nullptr;  // pinned host mirror
   uint32_t call_id = 0;
+  double depth_scale = 1.0;  // raw u16 depth units per metre (tsdf_table_set_depth_scale)
   // scratch (grown on demand, never shrunk)
   Buf in0, in1, dray, dcol, ends, flags, new_list, touched, work, pairs, pairs_alt, cub_tmp,
       ray_len, ray_nhat, ray_src, ray_rgb, block_sums, lists, cand, mesh_scratch;

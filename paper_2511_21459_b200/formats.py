@@ -161,6 +161,19 @@ def load_map(path, stream=None):
     return table, archive, info
 
 
+def read_points(path) -> np.ndarray:
+    """Points of a PLY (its vertices) or a whitespace-separated xyz text file
+    (formats.py:145-154)."""
+    path = Path(path)
+    if path.suffix.lower() == ".ply":
+        return read_mesh(path).vertices
+    try:
+        data = np.loadtxt(path, dtype=np.float64, ndmin=2)
+    except (OSError, ValueError) as exc:
+        raise FormatError(f"cannot read points from {path}: {exc}") from exc
+    return data[:, :3]
+
+
 # -- meshes (binary little-endian PLY, formats.py:33-120) -----------------------
 
 _PLY_VERTEX = np.dtype([("xyz", "<f4", (3,)), ("n", "<f4", (3,)), ("rgb", "u1", (3,))], align=False)

@@ -169,6 +169,14 @@ class HashTable:
         """Own only blocks whose key hashes to ``rank`` of ``world`` GPUs."""
         N.check(N.lib().tsdf_table_set_shard(self._h, int(rank), int(world)), "set_shard")
 
+    def set_depth_scale(self, depth_scale: float) -> None:
+        """Raw uint16 depth units per metre for the following depth calls
+        (z = raw / depth_scale in f64, datasets.py:108-113)."""
+        depth_scale = float(depth_scale)
+        if getattr(self, "_depth_scale", 1.0) != depth_scale:
+            N.check(N.lib().tsdf_table_set_depth_scale(self._h, depth_scale), "set_depth_scale")
+            self._depth_scale = depth_scale
+
     def reset(self) -> None:
         N.check(N.lib().tsdf_table_reset(self._h), "reset")
 

@@ -94,7 +94,7 @@ def _frame_keys_tau(table: HashTable, frame, tau: float) -> np.ndarray:
     n = C.c_int64()
     R, t = _pose(frame.pose)
     if isinstance(frame, DepthFrame):
-        dptr, ddt, dmem, _keep = N.as_buffer(frame.depth, (N.F64, N.F32))
+        dptr, ddt, dmem, _keep = _depth_buffer(table, frame)
         rc = N.lib().tsdf_depth_keys(table._h, dptr, ddt, frame.height, frame.width, dmem,
                                      frame.intrinsics.as_array(), R, t, float(tau),
                                      out.ctypes.data, cap, C.byref(n))
@@ -104,6 +104,18 @@ def _frame_keys_tau(table: HashTable, frame, tau: float) -> np.ndarray:
                                     float(tau), out.ctypes.data, cap, C.byref(n))
     N.check(rc, "frame_keys")
     return out[:n.value]
+
+
+def _depth_buffer(table: HashTable, frame, scale=None):
+    """as_buffer of the frame's depth.  Raw uint16 depth is scaled on the
+    device (z = raw / depth_scale in f64, datasets.py:108-113): the table's
+    depth scale is set to the frame's before the call."""
+    p, dt, m, k = N.as_buffer(frame.depth, (N.F64, N.F32, N.U16))
+    if dt == N.U16:
+        if scale is not None and frame.depth_scale != scale:
+            raise ValueError("frames of one window must share depth_scale")
+        table.set_depth_scale(frame.depth_scale)
+    return p, dt, m, k
 
 
 def _stats(st) -> IntegrationStats:
@@ -127,7 +139,7 @@ def integrate_depth(table: HashTable, frame: DepthFrame, tau: float, archive=Non
     if tau <= 0:
         raise ValueError("tau must be positive")
     _stream_in_for(table, frame, tau, archive)
-    dptr, ddt, dmem, _keep_d = N.as_buffer(frame.depth, (N.F64, N.F32))
+    dptr, ddt, dmem, _keep_d = _depth_buffer(table, frame)
     cptr, cdt, cmem, _keep_c = (None, 0, dmem, None)
     if frame.color is not None:
         cptr, cdt, cmem, _keep_c = N.as_buffer(frame.color, (N.F64, N.F32, N.U8))
@@ -155,7 +167,7 @@ def integrate_depth_walk(table: HashTable, frame: DepthFrame, tau: float, ray_ra
     integrate_depth_keys returns."""
     if tau <= 0:
         raise ValueError("tau must be positive")
-    dptr, ddt, dmem, _keep_d = N.as_buffer(frame.depth, (N.F64, N.F32))
+    dptr, ddt, dmem, _keep_d = _depth_buffer(table, frame)
     cptr, cdt, cmem, _keep_c = (None, 0, dmem, None)
     if frame.color is not None:
         cptr, cdt, cmem, _keep_c = N.as_buffer(frame.color, (N.F64, N.F32, N.U8))
@@ -241,7 +253,7 @@ def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial
     keep, dptrs, cptrs = [], [], []
     ddt = cdt = mem = None
     for f in frames:
-        p, dt, m, k = N.as_buffer(f.depth, (N.F64, N.F32))
+        p, dt, m, k = _depth_buffer(table, f, frames[0].depth_scale)
         keep.append(k)
         if ddt is None:
             ddt, mem = dt, m

@@ -84,42 +84,88 @@ class ShardedFusion:
         return int(t.item())
 
 
+_DTYPES = ("<f8", "<f4", "|u1", "<u2")
+
+
+class _DeviceView:
+    """A received device array: the broadcast byte tensor seen with the
+    sender's element type and shape (through __cuda_array_interface__, so
+    the kernels read it in place)."""
+
+    def __init__(self, raw, typestr, shape):
+        self._raw = raw
+        self.shape = tuple(shape)
+        self.__cuda_array_interface__ = {"data": (raw.data_ptr(), False), "shape": self.shape,
+                                         "typestr": typestr, "strides": None, "version": 2}
+
+
+def _bytes_of(a, torch, device):
+    """(uint8 tensor on `device`, typestr, shape) of a host or device array."""
+    if isinstance(a, torch.Tensor):
+        t = a.contiguous()
+        typestr = np.dtype(str(t.dtype).replace("torch.", "")).str
+        return t.reshape(-1).view(torch.uint8).to(device), typestr, tuple(t.shape)
+    cai = getattr(a, "__cuda_array_interface__", None)
+    if cai is not None:
+        t = torch.as_tensor(a, device=device).contiguous()
+        return t.reshape(-1).view(torch.uint8), np.dtype(cai["typestr"]).str, tuple(cai["shape"])
+    h = np.ascontiguousarray(a)
+    return torch.from_numpy(h.reshape(-1).view(np.uint8)).to(device), h.dtype.str, h.shape
+
+
+def _bcast_array(a, rank, dist, torch, group, device):
+    """Broadcast one array from rank 0 bit-for-bit in its own element type
+    (f64 / f32 / u8 / u16): a header of (type, rank, shape), then the bytes."""
+    head = torch.zeros(5, dtype=torch.int64, device=device)
+    raw = None
+    if rank == 0:
+        raw, typestr, shape = _bytes_of(a, torch, device)
+        if typestr not in _DTYPES:
+            raise ValueError(f"cannot broadcast arrays of type {typestr}")
+        head.copy_(torch.tensor([_DTYPES.index(typestr), len(shape)] + list(shape)
+                                + [0] * (3 - len(shape)), dtype=torch.int64))
+    dist.broadcast(head, 0, group=group)
+    code, nd, *dims = (int(x) for x in head.tolist())
+    shape, typestr = tuple(dims[:nd]), _DTYPES[code]
+    if rank != 0:
+        raw = torch.empty(int(np.prod(shape)) * np.dtype(typestr).itemsize, dtype=torch.uint8,
+                          device=device)
+    dist.broadcast(raw, 0, group=group)
+    if raw.is_cuda:
+        return _DeviceView(raw, typestr, shape)
+    return raw.numpy().view(np.dtype(typestr)).reshape(shape)
+
+
 def broadcast_frame(frame, dist, torch, group=None, device=None):
+    """Rank 0's frame on every rank: pose, intrinsics and depth scale, then
+    the depth (or points) and colour arrays in their own element types, so
+    every rank fuses exactly the values rank 0 was given."""
     from .geometry import DepthFrame, Intrinsics, PointCloudFrame, SensorPose
     rank = dist.get_rank(group)
-    is_depth = torch.tensor([1 if isinstance(frame, DepthFrame) else 0] if rank == 0 else [0],
-                            dtype=torch.int64, device=device)
-    dist.broadcast(is_depth, 0, group=group)
-    data = frame.depth if (rank == 0 and is_depth.item()) else (frame.points if rank == 0 else None)
-    meta = torch.zeros(16, dtype=torch.float64, device=device)
-    shape = torch.zeros(3, dtype=torch.int64, device=device)
-    has_col = torch.zeros(1, dtype=torch.int64, device=device)
+    flags = torch.zeros(2, dtype=torch.int64, device=device)
+    meta = torch.zeros(17, dtype=torch.float64, device=device)
     if rank == 0:
-        R, t = frame.pose.rotation.reshape(9), frame.pose.translation
-        k = frame.intrinsics.as_array() if is_depth.item() else np.zeros(4)
-        meta.copy_(torch.from_numpy(np.concatenate([R, t, k])))
-        shape.copy_(torch.tensor(list(np.asarray(data).shape) + [0] * (3 - np.asarray(data).ndim)))
-        col = frame.color if is_depth.item() else frame.colors
-        has_col[0] = 0 if col is None else 1
-    for x in (meta, shape, has_col):
-        dist.broadcast(x, 0, group=group)
-    shp = [int(s) for s in shape.tolist() if s]
-    buf = (torch.as_tensor(np.ascontiguousarray(data, dtype=np.float32), device=device) if rank == 0
-           else torch.empty(shp, dtype=torch.float32, device=device))
-    dist.broadcast(buf, 0, group=group)
-    col_t = None
-    if has_col.item():
-        csh = shp + [3] if is_depth.item() else [shp[0], 3]
-        col_t = (torch.as_tensor(np.ascontiguousarray(frame.color if is_depth.item() else frame.colors,
-                                                      dtype=np.float32), device=device)
-                 if rank == 0 else torch.empty(csh, dtype=torch.float32, device=device))
-        dist.broadcast(col_t, 0, group=group)
+        is_depth = isinstance(frame, DepthFrame)
+        col = frame.color if is_depth else frame.colors
+        flags.copy_(torch.tensor([int(is_depth), int(col is not None)], dtype=torch.int64))
+        k = frame.intrinsics.as_array() if is_depth else np.zeros(4)
+        scale = frame.depth_scale if is_depth else 1.0
+        meta.copy_(torch.from_numpy(np.concatenate([frame.pose.rotation.reshape(9),
+                                                    frame.pose.translation, k, [scale]])))
+    dist.broadcast(flags, 0, group=group)
+    dist.broadcast(meta, 0, group=group)
+    is_depth, has_col = (bool(x) for x in flags.tolist())
+    data = (frame.depth if is_depth else frame.points) if rank == 0 else None
+    arr = _bcast_array(data, rank, dist, torch, group, device)
+    carr = None
+    if has_col:
+        carr = _bcast_array((frame.color if is_depth else frame.colors) if rank == 0 else None,
+                            rank, dist, torch, group, device)
     m = meta.cpu().numpy()
     pose = SensorPose(m[:9].reshape(3, 3), m[9:12])
-    arr = buf if buf.is_cuda else buf.numpy()
-    carr = None if col_t is None else (col_t if col_t.is_cuda else col_t.numpy())
-    if is_depth.item():
-        return DepthFrame(depth=arr, intrinsics=Intrinsics(*m[12:16]), pose=pose, color=carr)
+    if is_depth:
+        return DepthFrame(depth=arr, intrinsics=Intrinsics(*m[12:16]), pose=pose, color=carr,
+                          depth_scale=float(m[16]))
     return PointCloudFrame(points=arr, pose=pose, colors=carr)
 
 

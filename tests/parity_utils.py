@@ -85,6 +85,13 @@ def array_digest(*arrs) -> str:
 # backends
 # ---------------------------------------------------------------------------
 
+def _metres(frame):
+    """f64 depth in metres as the reference frame holds it (raw uint16 depth
+    divided by its scale, datasets.py:113)."""
+    d = np.asarray(frame.depth, dtype=np.float64)
+    return d / frame.depth_scale if np.asarray(frame.depth).dtype == np.uint16 else d
+
+
 class RefBackend:
     name = "reference"
 
@@ -94,7 +101,7 @@ class RefBackend:
 
     def depth(self, frame, tau, weight_cap=0.0):
         from tsdfusion.geometry import DepthFrame, Intrinsics, SensorPose
-        f = DepthFrame(depth=np.asarray(frame.depth, dtype=np.float64),
+        f = DepthFrame(depth=_metres(frame),
                        intrinsics=Intrinsics(frame.intrinsics.fx, frame.intrinsics.fy,
                                              frame.intrinsics.cx, frame.intrinsics.cy),
                        pose=SensorPose(frame.pose.rotation, frame.pose.translation),
@@ -150,7 +157,7 @@ class OracleBackend:
 
     def depth(self, frame, tau, weight_cap=0.0):
         i = frame.intrinsics
-        s = self.t.integrate_depth(np.asarray(frame.depth, dtype=np.float64),
+        s = self.t.integrate_depth(_metres(frame),
                                    [i.fx, i.fy, i.cx, i.cy], frame.pose.rotation,
                                    frame.pose.translation, tau,
                                    color=None if frame.color is None else _color_f64(frame.color),

@@ -140,3 +140,54 @@ def test_two_rank_ray_sharded_key_exchange():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok and n > 0 for ok, n in res.values())
+
+
+def _broadcast_worker(rank, world, port, q):
+    """broadcast_frame keeps every array's element type and bits: f64 and
+    f32 depth, raw u16 depth with its scale, u8 / f64 colour, f32 points."""
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "tests"))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_21459_b200 import DepthFrame, synth
+    from paper_2511_21459_b200.sharding import broadcast_frame
+    from dataset_utils import SCALE, raw_depth
+    d64 = synth.render_frames("room", 1, 40, 30)[0]
+    d32 = synth.render_frames("room", 1, 40, 30, depth_dtype=np.float32, color_dtype=np.uint8)[0]
+    raw = DepthFrame(raw_depth(d32.depth), d32.intrinsics, d32.pose, color=d32.color,
+                     depth_scale=SCALE)
+    pts = synth.lidar_frames(1, 8, 64)[0]
+    pts.colors = np.arange(3 * len(pts.points), dtype=np.int64).reshape(-1, 3).astype(np.uint8)
+    ok = []
+    for f in (d64, d32, raw, pts):
+        g = broadcast_frame(f if rank == 0 else None, dist, torch)
+        a, b = (f.points, g.points) if hasattr(f, "points") else (f.depth, g.depth)
+        ca, cb = (f.colors, g.colors) if hasattr(f, "points") else (f.color, g.color)
+        same = (a.dtype == b.dtype and np.array_equal(a, b, equal_nan=True)
+                and ca.dtype == cb.dtype and np.array_equal(ca, cb)
+                and np.array_equal(f.pose.rotation, g.pose.rotation)
+                and np.array_equal(f.pose.translation, g.pose.translation))
+        if hasattr(f, "depth"):
+            same = same and g.depth_scale == f.depth_scale and g.intrinsics == f.intrinsics
+        ok.append(bool(same))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_two_rank_frame_broadcast_keeps_types():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_broadcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] == [True] * 4
