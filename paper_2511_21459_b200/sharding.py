@@ -77,6 +77,15 @@ class ShardedFusion:
         st = self.engine.integrate_frame(f)
         return combine_stats(st, self.dist, self.torch, self.group, self.device)
 
+    def extract(self, iso: float = 0.0, dst: int = 0):
+        """FusionEngine.extract over the whole map: the mesh on rank `dst`
+        (None elsewhere)."""
+        if self.world == 1:
+            return self.engine.extract(iso=iso)
+        cfg = self.engine.config
+        return extract_mesh_sharded(self.engine.table, self.dist, self.torch, self.group,
+                                    self.device, iso, cfg.collapse_epsilon_factor * cfg.nu_fine, dst)
+
     def maybe_merge(self):
         n = self.engine.maybe_merge()
         t = self.torch.tensor([n], dtype=self.torch.int64, device=self.device)
@@ -220,3 +229,82 @@ def integrate_depth_raysharded(table, frame, tau, dist, torch, group=None, devic
         setattr(st2, k, getattr(st1, k))
     st2.warnings = list(st1.warnings)
     return combine_stats(st2, dist, torch, group, device)
+
+
+# -- mesh extraction over shards ------------------------
+#
+# Corner sampling reads the 26 lattice neighbours of a block (meshing.py:
+# 94-158, 306-310), and with hash ownership nearly every neighbour of a block
+# lives on another rank, so a per-rank halo would be most of the map anyway.
+# The shards therefore gather their blocks (bulk level exports, packed in the
+# reference's block-record layout) onto one GPU, which rebuilds the map in a
+# scratch table and extracts it there.  The mesh depends only on map content
+# (never on heap handles), so it is bit-identical to extracting the
+# single-GPU table.  A large-room map is ~5 GB: one NVLink all-gather.
+
+def shard_records(table) -> bytes:
+    """This shard's live blocks: a header of per-level block counts (u64),
+    then the blocks as reference block records, level by level (canonical
+    order within a level)."""
+    from .formats import pack_records
+    counts, out = [], []
+    for level in range(table.num_levels):
+        coords, _, t, w, s2, col = table.export_level(level)
+        counts.append(len(coords))
+        if len(coords):
+            out.append(pack_records(level, coords, t, w, s2, col).tobytes())
+    return np.asarray([table.num_levels] + counts, dtype="<u8").tobytes() + b"".join(out)
+
+
+def table_from_records(blobs, like):
+    """A table with the hash geometry of `like` holding every block of the
+    shard_records blobs."""
+    from .formats import record_dtype
+    from .hashgrid import HashTable
+    per_level = {}
+    for blob in blobs:
+        nl = int(np.frombuffer(blob, "<u8", 1, 0)[0])
+        counts = np.frombuffer(blob, "<u8", nl, 8).astype(np.int64)
+        off = 8 * (nl + 1)
+        for level, n in enumerate(counts.tolist()):
+            if n:
+                dt = record_dtype(level)
+                per_level.setdefault(level, []).append(np.frombuffer(blob, dt, n, off))
+                off += n * dt.itemsize
+    caps = [max(1, sum(len(r) for r in per_level.get(l, []))) for l in range(like.num_levels)]
+    t = HashTable(like.n_hash, like.bucket_capacity, like.overflow_capacity, like.block_edge,
+                  heap_capacities=tuple(caps))
+    for level, recs in sorted(per_level.items()):
+        r = np.concatenate(recs)
+        t.import_blocks(level, r["coord"], r["tsdf"], r["weight"], r["s2"], r["color"])
+    return t
+
+
+def _gather_bytes(blob: bytes, dst: int, dist, torch, group=None, device=None):
+    """Every rank's byte string on rank `dst` (None elsewhere): lengths,
+    then one padded all-gather (NCCL has no variable-size gather)."""
+    world = dist.get_world_size(group)
+    n = torch.tensor([len(blob)], dtype=torch.int64, device=device)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    cap = max(1, max(sizes))
+    buf = torch.zeros(cap, dtype=torch.uint8, device=device)
+    if blob:
+        buf[:len(blob)] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(device)
+    parts = [torch.empty(cap, dtype=torch.uint8, device=device) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    if dist.get_rank(group) != dst:
+        return None
+    return [bytes(p[:s].cpu().numpy().tobytes()) for p, s in zip(parts, sizes)]
+
+
+def extract_mesh_sharded(table, dist, torch, group=None, device=None, iso: float = 0.0,
+                         collapse_epsilon=None, dst: int = 0):
+    """extract_mesh over the union of the shards' tables: the Mesh on rank
+    `dst`, None on the other ranks."""
+    from .meshing import extract_mesh
+    blobs = _gather_bytes(shard_records(table), dst, dist, torch, group, device)
+    if blobs is None:
+        return None
+    return extract_mesh(table_from_records(blobs, table), iso=iso, collapse_epsilon=collapse_epsilon)

@@ -514,3 +514,34 @@ def test_merge_memo_respects_parameter_changes():
                 out.append(b.merge(sigma, all_levels=al))
         results[name] = (out, PU.state_digest(b.state()))
     assert results["gpu"] == results["oracle"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_extraction_equals_single_gpu(world):
+    """Mesh extraction over block-key shards: the shards'
+    blocks gathered as reference block records into one table extract the
+    single-GPU mesh bit for bit (with and without vertex collapse)."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    from paper_2511_21459_b200.sharding import shard_records, table_from_records
+    frames = synth.render_frames("room", 20, 128, 96, depth_dtype=np.float32, color_dtype=np.uint8)
+    full = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000, 5000))
+    shards = []
+    for r in range(world):
+        t = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000, 5000))
+        t.set_shard(r, world)
+        shards.append(t)
+    for i, f in enumerate(frames):
+        for t in [full] + shards:
+            P.integrate_depth(t, f, 0.015)
+        if (i + 1) % 10 == 0:
+            for t in [full] + shards:
+                P.apply_merges(t, 2.5e-5, all_levels=True)
+    assert full.heaps[1].occupied > 0
+    g = table_from_records([shard_records(t) for t in shards], full)
+    for eps in (None, 0.0025):
+        a, b = P.extract_mesh(full, collapse_epsilon=eps), P.extract_mesh(g, collapse_epsilon=eps)
+        assert a.num_triangles > 1000
+        for x, y in ((a.vertices, b.vertices), (a.normals, b.normals), (a.colors, b.colors),
+                     (a.triangles, b.triangles)):
+            assert np.array_equal(x, y)

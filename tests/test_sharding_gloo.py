@@ -191,3 +191,34 @@ def test_two_rank_frame_broadcast_keeps_types():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0] == res[1] == [True] * 4
+
+
+def _gather_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_21459_b200.sharding import _gather_bytes
+    blob = bytes(range(rank * 7 % 256)) * (rank + 1)  # rank 0 sends nothing
+    got = _gather_bytes(blob, 1, dist, torch)
+    q.put((rank, got))
+    dist.destroy_process_group()
+
+
+def test_three_rank_variable_size_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] is None and res[2] is None
+    assert res[1] == [bytes(range(r * 7 % 256)) * (r + 1) for r in range(3)]
