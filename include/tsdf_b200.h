@@ -187,6 +187,24 @@ void tsdf_mesh_free(tsdf_mesh *m);
 int tsdf_nn_distance(const double *tree, int64_t n_tree, const double *query, int64_t n_query,
                      int32_t mem, double *dist, void *cuda_stream);
 
+/* build_quadtree(image, contrast_threshold, min_pixel) -- quadtree.py:94-109.
+ * image: H*W*3 f64 (host or device per mem).  Writes the leaves in the
+ * reference's breadth-first order as (x0, y0, w, h) int32 quadruples and
+ * their contrasts; both outputs are host arrays with room for H*W leaves. */
+int tsdf_quadtree_build(const double *image, int32_t height, int32_t width, int32_t mem,
+                        double threshold, int32_t min_pixel, int32_t *leaves_out,
+                        double *contrast_out, int64_t *n_leaves, void *cuda_stream);
+/* seed_splats(leaves, DepthFrame) -- quadtree.py:112-148.  One splat per
+ * leaf with valid depth at its centre: world position (3 f64), scale
+ * w * d / fx, mean colour (0.5 grey without rgb); valid_out[i] says whether
+ * leaf i produced a splat.  depth: f64 / f32 metres or u16 raw / depth_scale;
+ * rgb: f64 / f32 in [0, 1] or u8 (/ 255) or NULL.  Outputs are host arrays. */
+int tsdf_seed_splats(const int32_t *leaves, int64_t n, const void *depth, int32_t depth_dtype,
+                     double depth_scale, const void *rgb, int32_t rgb_dtype, int32_t height,
+                     int32_t width, int32_t mem, const double *K, const double *R,
+                     const double *trans, double *pos_out, double *scale_out, double *color_out,
+                     uint8_t *valid_out, void *cuda_stream);
+
 /* HashTable.find_batch (hashgrid.py:300-331) */
 int tsdf_find_batch(tsdf_table *t, const int64_t *coords, int64_t n, int64_t *handles,
                     int32_t *levels, uint8_t *found);

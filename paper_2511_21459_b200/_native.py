@@ -94,6 +94,9 @@ def lib():
     L.tsdf_extract_mesh.argtypes = [_ptr, dbl, dbl, C.POINTER(MeshC)]
     L.tsdf_mesh_free.argtypes = [C.POINTER(MeshC)]
     L.tsdf_nn_distance.argtypes = [_ptr, i64, _ptr, i64, i32, _ptr, _ptr]
+    L.tsdf_quadtree_build.argtypes = [_ptr, i32, i32, i32, dbl, i32, _ptr, _ptr, C.POINTER(i64), _ptr]
+    L.tsdf_seed_splats.argtypes = [_ptr, i64, _ptr, i32, dbl, _ptr, i32, i32, i32, i32, _f64p, _f64p,
+                                   _f64p, _ptr, _ptr, _ptr, _ptr, _ptr]
     L.tsdf_find_batch.argtypes = [_ptr, _i64p, i64, _i64p, np.ctypeslib.ndpointer(np.int32),
                                   np.ctypeslib.ndpointer(np.uint8)]
     L.tsdf_insert.argtypes = [_ptr, _i64p, i32, C.POINTER(i64)]
