@@ -70,7 +70,7 @@ struct Table {
     const void* rgb = nullptr;  // device colour of the frame (staged or caller-owned)
     Counters* c = nullptr;
     uint32_t* abort_word = nullptr;
-    double f[20];               // FrameDev image
+    double f[24];               // FrameDev image
   } shf;
   Frame shf_frame{};
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
