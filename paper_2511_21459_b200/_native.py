@@ -147,11 +147,24 @@ def device_info():
     return a.value, b.value, c.value
 
 
+_CODES = {np.dtype(np.float64): F64, np.dtype(np.float32): F32, np.dtype(np.uint8): U8,
+          np.dtype(np.uint16): U16}
+_TORCH_CODES = {"torch.float64": F64, "torch.float32": F32, "torch.uint8": U8, "torch.uint16": U16}
+
+
 def as_buffer(arr, allowed):
     """(pointer, dtype code, mem kind, keepalive) for a numpy array or a CUDA
     array (anything exposing __cuda_array_interface__, e.g. a torch tensor)."""
-    codes = {np.dtype(np.float64): F64, np.dtype(np.float32): F32, np.dtype(np.uint8): U8,
-             np.dtype(np.uint16): U16}
+    codes = _CODES
+    if type(arr).__module__ == "torch" and arr.is_cuda:
+        # fast path: a torch tensor's __cuda_array_interface__ is rebuilt on
+        # every access, which costs more than a frame's enqueue
+        code = _TORCH_CODES.get(str(arr.dtype))
+        if code is None or code not in allowed:
+            raise ValueError(f"unsupported device dtype {arr.dtype}")
+        if not arr.is_contiguous():
+            raise ValueError("device arrays must be C-contiguous")
+        return arr.data_ptr(), code, MEM_DEVICE, arr
     cai = getattr(arr, "__cuda_array_interface__", None)
     if cai is not None:
         dt = np.dtype(cai["typestr"])
