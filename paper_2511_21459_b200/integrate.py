@@ -252,12 +252,14 @@ def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial
     n = len(frames)
     keep, dptrs, cptrs = [], [], []
     ddt = cdt = mem = None
+    H, W = frames[0].height, frames[0].width
+    scale0 = frames[0].depth_scale
     for f in frames:
-        p, dt, m, k = _depth_buffer(table, f, frames[0].depth_scale)
+        p, dt, m, k = _depth_buffer(table, f, scale0)
         keep.append(k)
         if ddt is None:
             ddt, mem = dt, m
-        if dt != ddt or m != mem or (f.height, f.width) != (frames[0].height, frames[0].width):
+        if dt != ddt or m != mem or tuple(f.depth.shape) != (H, W):
             raise ValueError("integrate_depth_batch: frames must share size, dtype and memory kind")
         dptrs.append(p)
         if f.color is not None:
@@ -270,9 +272,10 @@ def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial
             cptrs.append(cp)
     if cptrs and len(cptrs) != n:
         raise ValueError("integrate_depth_batch: either every frame has colour or none")
-    K = np.concatenate([f.intrinsics.as_array() for f in frames])
-    R = np.concatenate([np.ascontiguousarray(f.pose.rotation, dtype=np.float64).reshape(9) for f in frames])
-    T = np.concatenate([np.ascontiguousarray(f.pose.translation, dtype=np.float64).reshape(3) for f in frames])
+    K = np.array([(f.intrinsics.fx, f.intrinsics.fy, f.intrinsics.cx, f.intrinsics.cy) for f in frames],
+                 dtype=np.float64).reshape(-1)
+    R = np.concatenate([f.pose.rotation.reshape(9) for f in frames])  # f64, C-contiguous (SensorPose)
+    T = np.concatenate([f.pose.translation for f in frames])
     darr = (C.c_void_p * n)(*dptrs)
     carr = (C.c_void_p * n)(*cptrs) if cptrs else None
     st = (N.IntegrationStatsC * n)()
@@ -280,7 +283,7 @@ def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial
     ms = N.MergeStatsC()
     sig, frac, minw, alll = merge if merge is not None else (0.0, 0.0, 0.0, False)
     rc = N.lib().tsdf_integrate_depth_window(table._h, n, darr, ddt, carr, cdt or 0,
-                                             frames[0].height, frames[0].width, mem, K, R, T,
+                                             H, W, mem, K, R, T,
                                              float(tau), float(weight_cap), st, C.byref(done),
                                              float(sig), float(frac), float(minw), int(bool(alll)),
                                              float(fill_limit),
