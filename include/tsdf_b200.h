@@ -177,6 +177,14 @@ int tsdf_apply_merges(tsdf_table *t, double sigma_threshold, double min_eligible
  * collapse_epsilon < 0 selects the default 0.25 * voxel_size(0). */
 int tsdf_extract_mesh(tsdf_table *t, double iso, double collapse_epsilon, tsdf_mesh *out);
 void tsdf_mesh_free(tsdf_mesh *m);
+/* Two-phase extract_mesh: _begin runs the extraction and keeps the mesh on
+ * the device (returns its sizes); _read copies it straight into caller-owned
+ * host arrays (vertices / normals / colours nv x 3 f64, triangles nt x 3
+ * i64) -- no intermediate host copy.  Same mesh as tsdf_extract_mesh. */
+int tsdf_extract_mesh_begin(tsdf_table *t, double iso, double eps, int64_t *num_vertices,
+                            int64_t *num_triangles);
+int tsdf_extract_mesh_read(tsdf_table *t, double *vertices, double *normals, double *colors,
+                           int64_t *triangles);
 
 /* Nearest-neighbour distance from every query point to the tree point set
  * (FP64, sqrt((dx*dx + dy*dy) + dz*dz), exact): the cKDTree(tree).query(q,

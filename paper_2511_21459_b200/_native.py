@@ -93,6 +93,8 @@ def lib():
     L.tsdf_apply_merges.argtypes = [_ptr, dbl, dbl, dbl, i32, C.POINTER(MergeStatsC)]
     L.tsdf_extract_mesh.argtypes = [_ptr, dbl, dbl, C.POINTER(MeshC)]
     L.tsdf_mesh_free.argtypes = [C.POINTER(MeshC)]
+    L.tsdf_extract_mesh_begin.argtypes = [_ptr, dbl, dbl, C.POINTER(i64), C.POINTER(i64)]
+    L.tsdf_extract_mesh_read.argtypes = [_ptr, _ptr, _ptr, _ptr, _ptr]
     L.tsdf_nn_distance.argtypes = [_ptr, i64, _ptr, i64, i32, _ptr, _ptr]
     L.tsdf_quadtree_build.argtypes = [_ptr, i32, i32, i32, dbl, i32, _ptr, _ptr, C.POINTER(i64), _ptr]
     L.tsdf_seed_splats.argtypes = [_ptr, i64, _ptr, i32, dbl, _ptr, i32, i32, i32, i32, _f64p, _f64p,

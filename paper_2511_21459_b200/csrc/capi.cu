@@ -235,6 +235,19 @@ int tsdf_extract_mesh(tsdf_table* t, double iso, double eps, tsdf_mesh* out) {
   return s;
 }
 
+int tsdf_extract_mesh_begin(tsdf_table* t, double iso, double eps, int64_t* num_vertices,
+                            int64_t* num_triangles) {
+  NEED(t);
+  if (eps < 0) eps = 0.25 * (T_(t)->d.edge / kFineSide);
+  return extract_mesh_begin(T_(t), iso, eps, num_vertices, num_triangles);
+}
+
+int tsdf_extract_mesh_read(tsdf_table* t, double* vertices, double* normals, double* colors,
+                           int64_t* triangles) {
+  NEED(t);
+  return extract_mesh_read(T_(t), vertices, normals, colors, triangles);
+}
+
 void tsdf_mesh_free(tsdf_mesh* m) {
   if (!m) return;
   MeshOut o{m->vertices, m->normals, m->colors, m->num_vertices, m->triangles, m->num_triangles};

@@ -44,6 +44,8 @@ struct Table {
   Counters* hcnt = nullptr;  // pinned host mirror
   uint32_t call_id = 0;
   double depth_scale = 1.0;  // raw u16 depth units per metre (tsdf_table_set_depth_scale)
+  Buf mesh_out;                   // the last extract_mesh_begin result (device)
+  int64_t mesh_nv = -1, mesh_nt = 0;
   // scratch (grown on demand, never shrunk)
   Buf in0, in1, dray, dcol, ends, flags, new_list, touched, work, pairs, pairs_alt, cub_tmp,
       ray_len, ray_nhat, ray_src, ray_rgb, block_sums, lists, cand, mesh_scratch;
@@ -188,6 +190,8 @@ int collapse_vertices(const double* v, const double* n, const double* c, int64_t
 
 // mesh extraction (mesh.cu)
 int extract_mesh(Table* T, double iso, double eps, MeshOut* out);
+int extract_mesh_begin(Table* T, double iso, double eps, int64_t* nv, int64_t* nt);
+int extract_mesh_read(Table* T, double* v, double* n, double* c, int64_t* tri);
 void mesh_free(MeshOut* m);
 
 }  // namespace tsdf

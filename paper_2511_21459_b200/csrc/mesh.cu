@@ -637,6 +637,53 @@ __global__ void k_compact_tris(const int64_t* tri, const int64_t* keep, const in
 }
 
 // ---------------------------------------------------------------------------
+// chunk bookkeeping on the device (was a host loop over every kept block):
+// the blocks of level l occupy [loff[l], loff[l] + n[l]) in canonical order,
+// cut into chunks of 256 numbered from cbase[l]
+struct ChunkMeta {
+  int64_t loff[kMaxLevels + 1], cbase[kMaxLevels];
+  int n_levels;
+};
+__global__ void k_chunk_meta(ChunkMeta M, uint64_t nb, int64_t* chunk_of, int32_t* blevel,
+                             int64_t* chunk_start, int32_t* chunk_size) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < M.n_levels && (int64_t)i >= M.loff[l + 1]) l++;
+    const int64_t li = (int64_t)i - M.loff[l], n = M.loff[l + 1] - M.loff[l];
+    const int64_t G = M.cbase[l] + li / 256;
+    chunk_of[i] = G;
+    blevel[i] = l;
+    if (li % 256 == 0) {
+      chunk_start[G] = (int64_t)i;
+      chunk_size[G] = (int32_t)(n - li < 256 ? n - li : 256);
+    }
+  }
+}
+// a chunk emits if any of its blocks does (pass A's emit_any)
+__global__ void k_chunk_emits(const uint8_t* emit_any, const int64_t* chunk_of, uint64_t nb,
+                              uint8_t* chunk_emits) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (emit_any[i]) chunk_emits[chunk_of[i]] = 1;
+}
+// pass A's per-block counts laid out in emission order -- chunk by chunk,
+// then slot k of K (axis / triangle case), then block within the chunk --
+// and zeroed for chunks that emit nothing; an exclusive scan of this is
+// pass B's offsets
+__global__ void k_emit_order(const int32_t* cnt, int K, const int64_t* chunk_of,
+                             const int64_t* chunk_start, const int32_t* chunk_size,
+                             const uint8_t* chunk_emits, uint64_t nb, int64_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb * K;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = i / K;
+    const int k = (int)(i % K);
+    const int64_t G = chunk_of[b], cs = chunk_start[G];
+    const int64_t pos = K * cs + (int64_t)k * chunk_size[G] + ((int64_t)b - cs);
+    out[pos] = chunk_emits[G] ? cnt[i] : 0;
+  }
+}
+
 // host orchestration
 // ---------------------------------------------------------------------------
 
@@ -721,10 +768,49 @@ static int unique_rows(Scratch& S, const T* rows, uint64_t n, uint64_t* idx, int
 }
 
 // collapse + compaction on device arrays (consumes v/n/c/tri); fills host out
+// a mesh in device memory: vertices, normals, colours (nv x 3 f64 each)
+// then triangles (nt x 3 i64), one allocation in that order
+struct DevMesh {
+  char* base = nullptr;
+  int64_t nv = 0, nt = 0;
+  double* v() const { return (double*)base; }
+  double* n() const { return v() + 3 * nv; }
+  double* c() const { return n() + 3 * nv; }
+  int64_t* tri() const { return (int64_t*)(c() + 3 * nv); }
+  static size_t bytes(int64_t nv, int64_t nt) { return (size_t)nv * 72 + (size_t)nt * 24 + 64; }
+};
+
+// D2H of a device mesh into caller-owned host arrays
+static int mesh_to_host(const DevMesh& m, cudaStream_t st, double* v, double* n, double* c, int64_t* tri) {
+  if (m.nv) {
+    MCK(cudaMemcpyAsync(v, m.v(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(n, m.n(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(c, m.c(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+  }
+  if (m.nt) MCK(cudaMemcpyAsync(tri, m.tri(), m.nt * 24, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  return kOk;
+}
+
+// ... into malloc'd arrays (the MeshOut of tsdf_extract_mesh / collapse)
+static int mesh_to_malloc(const DevMesh& m, cudaStream_t st, MeshOut* out) {
+  memset(out, 0, sizeof(*out));
+  if (m.nv == 0 && m.nt == 0) return kOk;
+  out->nv = m.nv;
+  out->nt = m.nt;
+  out->v = (double*)malloc(std::max<int64_t>(m.nv, 1) * 24);
+  out->n = (double*)malloc(std::max<int64_t>(m.nv, 1) * 24);
+  out->c = (double*)malloc(std::max<int64_t>(m.nv, 1) * 24);
+  out->tri = (int64_t*)malloc(std::max<int64_t>(m.nt, 1) * 24);
+  return mesh_to_host(m, st, out->v, out->n, out->c, out->tri);
+}
+
+// collapse + compaction on device arrays (consumes v/n/c/tri); the result
+// lands in `keep` (a table-owned buffer) or in the scratch
 static int collapse_device(Scratch& S, const double* v, const double* nrm, const double* col,
                            uint64_t nv, const int64_t* tri, uint64_t nt, double eps,
-                           cudaStream_t st, MeshOut* out) {
-  memset(out, 0, sizeof(*out));
+                           cudaStream_t st, DevMesh* out, Buf* keep) {
+  *out = DevMesh{};
   if (nv == 0) return kOk;
   uint64_t* idx = S.bufs.get<uint64_t>(nv);
   int64_t* inv = S.bufs.get<int64_t>(nv);
@@ -744,51 +830,41 @@ static int collapse_device(Scratch& S, const double* v, const double* nrm, const
   double* cn = S.bufs.get<double>(3 * ng);
   double* cc = S.bufs.get<double>(3 * ng);
   int64_t* tri2 = S.bufs.get<int64_t>(3 * nt);
-  int64_t* keep = S.bufs.get<int64_t>(nt);
+  int64_t* keep_t = S.bufs.get<int64_t>(nt);
   int64_t* kpos = S.bufs.get<int64_t>(nt);
   uint8_t* used8 = S.bufs.get<uint8_t>(ng);
   int64_t* used = S.bufs.get<int64_t>(ng);
   int64_t* remap = S.bufs.get<int64_t>(ng);
-  if (!cv || !cn || !cc || !tri2 || !keep || !kpos || !used8 || !used || !remap) return kCapacityError;
+  if (!cv || !cn || !cc || !tri2 || !keep_t || !kpos || !used8 || !used || !remap) return kCapacityError;
   k_collapse_out<<<gridn(ng), 256, 0, st>>>(v, nrm, col, idx, gst, ng, nv, exact, cv, cn, cc);
   MCK(cudaMemsetAsync(used8, 0, ng, st));
-  if (nt) k_tri_filter<<<gridn(nt), 256, 0, st>>>(tri, inv, nt, cv, tri2, keep, used8);
+  if (nt) k_tri_filter<<<gridn(nt), 256, 0, st>>>(tri, inv, nt, cv, tri2, keep_t, used8);
   k_u8_to_i64<<<gridn(ng), 256, 0, st>>>(used8, ng, nt == 0, used);
   if (int s = exclusive_scan(S, used, remap, ng, st)) return s;
   int64_t last_r, last_u, last_p = 0, last_k = 0;
   MCK(cudaMemcpyAsync(&last_r, remap + ng - 1, 8, cudaMemcpyDeviceToHost, st));
   MCK(cudaMemcpyAsync(&last_u, used + ng - 1, 8, cudaMemcpyDeviceToHost, st));
   if (nt) {
-    if (int s = exclusive_scan(S, keep, kpos, nt, st)) return s;
+    if (int s = exclusive_scan(S, keep_t, kpos, nt, st)) return s;
     MCK(cudaMemcpyAsync(&last_p, kpos + nt - 1, 8, cudaMemcpyDeviceToHost, st));
-    MCK(cudaMemcpyAsync(&last_k, keep + nt - 1, 8, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(&last_k, keep_t + nt - 1, 8, cudaMemcpyDeviceToHost, st));
   }
   MCK(cudaStreamSynchronize(st));
   int64_t nu = last_r + last_u, ntk = last_p + last_k;
-  double* fv = S.bufs.get<double>(3 * nu);
-  double* fn = S.bufs.get<double>(3 * nu);
-  double* fc = S.bufs.get<double>(3 * nu);
-  int64_t* ft = S.bufs.get<int64_t>(3 * ntk);
-  if (!fv || !fn || !fc || !ft) return kCapacityError;
-  k_compact_verts<<<gridn(ng), 256, 0, st>>>(cv, cn, cc, used, remap, ng, fv, fn, fc);
-  if (nt) k_compact_tris<<<gridn(nt), 256, 0, st>>>(tri2, keep, kpos, remap, nt, ft);
+  DevMesh m;
+  m.nv = nu;
+  m.nt = ntk;
+  m.base = keep ? (char*)grow(*keep, DevMesh::bytes(nu, ntk)) : S.bufs.get<char>(DevMesh::bytes(nu, ntk));
+  if (!m.base) return kCapacityError;
+  k_compact_verts<<<gridn(ng), 256, 0, st>>>(cv, cn, cc, used, remap, ng, m.v(), m.n(), m.c());
+  if (nt) k_compact_tris<<<gridn(nt), 256, 0, st>>>(tri2, keep_t, kpos, remap, nt, m.tri());
   MCK(cudaGetLastError());
-  out->nv = nu;
-  out->nt = ntk;
-  out->v = (double*)malloc(std::max<int64_t>(nu, 1) * 24);
-  out->n = (double*)malloc(std::max<int64_t>(nu, 1) * 24);
-  out->c = (double*)malloc(std::max<int64_t>(nu, 1) * 24);
-  out->tri = (int64_t*)malloc(std::max<int64_t>(ntk, 1) * 24);
-  MCK(cudaMemcpyAsync(out->v, fv, nu * 24, cudaMemcpyDeviceToHost, st));
-  MCK(cudaMemcpyAsync(out->n, fn, nu * 24, cudaMemcpyDeviceToHost, st));
-  MCK(cudaMemcpyAsync(out->c, fc, nu * 24, cudaMemcpyDeviceToHost, st));
-  MCK(cudaMemcpyAsync(out->tri, ft, ntk * 24, cudaMemcpyDeviceToHost, st));
-  MCK(cudaStreamSynchronize(st));
+  *out = m;
   return kOk;
 }
 
-int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
-  memset(out, 0, sizeof(*out));
+static int extract_mesh_dev(Table* T, double iso, double eps, DevMesh* out) {
+  *out = DevMesh{};
   if (eps < 0) {
     set_error("epsilon must be non-negative");
     return kValueError;
@@ -838,30 +914,28 @@ int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
   uint32_t* sslots = S.bufs.get<uint32_t>(nb);
   int32_t* blevel = S.bufs.get<int32_t>(nb);
   if (!skeys || !sslots || !blevel) return kCapacityError;
-  std::vector<int64_t> h_chunk_of(nb), h_chunk_start;
-  std::vector<int32_t> h_chunk_size, h_blevel(nb);
-  uint64_t off = 0;
-  for (int l = 0; l < d.n_levels; l++) {
-    uint64_t n = hcnt[l];
-    if (!n) continue;
-    size_t b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, kkeys + l * cap, skeys + off, kslots + l * cap,
-                                    sslots + off, (int64_t)n, 0, 63, st);
-    if (int s = S.need(b)) return s;
-    MCK(cub::DeviceRadixSort::SortPairs(S.tmp, b, kkeys + l * cap, skeys + off, kslots + l * cap,
-                                        sslots + off, (int64_t)n, 0, 63, st));
-    int64_t chunk_base = (int64_t)h_chunk_start.size();
-    for (uint64_t i = 0; i < n; i += 256) {
-      h_chunk_start.push_back((int64_t)(off + i));
-      h_chunk_size.push_back((int32_t)std::min<uint64_t>(256, n - i));
+  ChunkMeta CM{};
+  CM.n_levels = d.n_levels;
+  uint64_t nchunks = 0;
+  {
+    uint64_t off = 0;
+    for (int l = 0; l < d.n_levels; l++) {
+      const uint64_t n = hcnt[l];
+      CM.loff[l] = (int64_t)off;
+      CM.cbase[l] = (int64_t)nchunks;
+      if (n) {
+        size_t b = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, b, kkeys + l * cap, skeys + off, kslots + l * cap,
+                                        sslots + off, (int64_t)n, 0, 63, st);
+        if (int s = S.need(b)) return s;
+        MCK(cub::DeviceRadixSort::SortPairs(S.tmp, b, kkeys + l * cap, skeys + off, kslots + l * cap,
+                                            sslots + off, (int64_t)n, 0, 63, st));
+      }
+      off += n;
+      nchunks += (n + 255) / 256;
     }
-    for (uint64_t i = 0; i < n; i++) {
-      h_chunk_of[off + i] = chunk_base + (int64_t)(i / 256);
-      h_blevel[off + i] = l;
-    }
-    off += n;
+    CM.loff[d.n_levels] = (int64_t)off;
   }
-  uint64_t nchunks = h_chunk_start.size();
   int64_t* chunk_of = S.bufs.get<int64_t>(nb);
   int64_t* chunk_start = S.bufs.get<int64_t>(nchunks);
   int32_t* chunk_size = S.bufs.get<int32_t>(nchunks);
@@ -870,10 +944,7 @@ int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
   uint8_t* emit_any = S.bufs.get<uint8_t>(nb);
   if (!chunk_of || !chunk_start || !chunk_size || !edge_cnt || !tri_cnt || !emit_any)
     return kCapacityError;
-  MCK(cudaMemcpyAsync(chunk_of, h_chunk_of.data(), nb * 8, cudaMemcpyHostToDevice, st));
-  MCK(cudaMemcpyAsync(chunk_start, h_chunk_start.data(), nchunks * 8, cudaMemcpyHostToDevice, st));
-  MCK(cudaMemcpyAsync(chunk_size, h_chunk_size.data(), nchunks * 4, cudaMemcpyHostToDevice, st));
-  MCK(cudaMemcpyAsync(blevel, h_blevel.data(), nb * 4, cudaMemcpyHostToDevice, st));
+  k_chunk_meta<<<gridn(nb), 256, 0, st>>>(CM, nb, chunk_of, blevel, chunk_start, chunk_size);
   McArgs A{};
   A.t = d;
   A.slots = sslots;
@@ -897,45 +968,36 @@ int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
   }
   T->launches++;
   MCK(cudaGetLastError());
-  // emission-order count sequences (host: small per-block arrays)
-  std::vector<int32_t> he(nb * 3), ht(nb * 5);
-  std::vector<uint8_t> hany(nb);
-  MCK(cudaMemcpyAsync(he.data(), edge_cnt, nb * 12, cudaMemcpyDeviceToHost, st));
-  MCK(cudaMemcpyAsync(ht.data(), tri_cnt, nb * 20, cudaMemcpyDeviceToHost, st));
-  MCK(cudaMemcpyAsync(hany.data(), emit_any, nb, cudaMemcpyDeviceToHost, st));
-  MCK(cudaStreamSynchronize(st));
-  std::vector<uint8_t> hce(nchunks, 0);
-  for (uint64_t b = 0; b < nb; b++) hce[h_chunk_of[b]] |= hany[b];
-  std::vector<int64_t> hvoff(nb * 3), htoff(nb * 5);
-  int64_t vtot = 0, ttot = 0;
-  for (uint64_t G = 0; G < nchunks; G++) {
-    int64_t cs = h_chunk_start[G], sz = h_chunk_size[G];
-    for (int a = 0; a < 3; a++)
-      for (int64_t b = 0; b < sz; b++) {
-        hvoff[3 * cs + a * sz + b] = vtot;
-        if (hce[G]) vtot += he[(cs + b) * 3 + a];
-      }
-    for (int k3 = 0; k3 < 5; k3++)
-      for (int64_t b = 0; b < sz; b++) {
-        htoff[5 * cs + k3 * sz + b] = ttot;
-        if (hce[G]) ttot += ht[(cs + b) * 5 + k3];
-      }
-  }
-  if (ttot == 0) return kOk;  // reference: no triangles -> empty mesh
+  // emission-order offsets for pass B, on the device
   uint8_t* chunk_emits = S.bufs.get<uint8_t>(nchunks);
+  int64_t* ecnt = S.bufs.get<int64_t>(nb * 3);
+  int64_t* tcnt = S.bufs.get<int64_t>(nb * 5);
   int64_t* voff = S.bufs.get<int64_t>(nb * 3);
   int64_t* toff = S.bufs.get<int64_t>(nb * 5);
+  if (!chunk_emits || !ecnt || !tcnt || !voff || !toff) return kCapacityError;
+  MCK(cudaMemsetAsync(chunk_emits, 0, nchunks, st));
+  k_chunk_emits<<<gridn(nb), 256, 0, st>>>(emit_any, chunk_of, nb, chunk_emits);
+  k_emit_order<<<gridn(nb * 3), 256, 0, st>>>(edge_cnt, 3, chunk_of, chunk_start, chunk_size, chunk_emits, nb, ecnt);
+  k_emit_order<<<gridn(nb * 5), 256, 0, st>>>(tri_cnt, 5, chunk_of, chunk_start, chunk_size, chunk_emits, nb, tcnt);
+  if (int s = exclusive_scan(S, ecnt, voff, nb * 3, st)) return s;
+  if (int s = exclusive_scan(S, tcnt, toff, nb * 5, st)) return s;
+  int64_t tails[4];
+  MCK(cudaMemcpyAsync(&tails[0], voff + nb * 3 - 1, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(&tails[1], ecnt + nb * 3 - 1, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(&tails[2], toff + nb * 5 - 1, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaMemcpyAsync(&tails[3], tcnt + nb * 5 - 1, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  const int64_t vtot = tails[0] + tails[1], ttot = tails[2] + tails[3];
+  T->launches += 5;
+  if (ttot == 0) return kOk;  // reference: no triangles -> empty mesh
   double* vpos = S.bufs.get<double>(3 * vtot);
   double* vnrm = S.bufs.get<double>(3 * vtot);
   double* vcol = S.bufs.get<double>(3 * vtot);
   int64_t* tri = S.bufs.get<int64_t>(3 * ttot);
-  if (!chunk_emits || !voff || !toff || !vpos || !vnrm || !vcol || !tri) {
+  if (!vpos || !vnrm || !vcol || !tri) {
     set_error("device allocation failed for mesh output");
     return kCapacityError;
   }
-  MCK(cudaMemcpyAsync(chunk_emits, hce.data(), nchunks, cudaMemcpyHostToDevice, st));
-  MCK(cudaMemcpyAsync(voff, hvoff.data(), nb * 24, cudaMemcpyHostToDevice, st));
-  MCK(cudaMemcpyAsync(toff, htoff.data(), nb * 40, cudaMemcpyHostToDevice, st));
   A.chunk_emits = chunk_emits;
   A.voff = voff;
   A.toff = toff;
@@ -968,9 +1030,46 @@ int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
   k_orient<<<gridn(nt), 256, 0, st>>>(tri, inv, nt, mv, mn, mt);
   T->launches += 12;
   MCK(cudaGetLastError());
-  int s = collapse_device(S, mv, mn, mc, (uint64_t)ng, mt, nt, eps, st, out);
+  int s = collapse_device(S, mv, mn, mc, (uint64_t)ng, mt, nt, eps, st, out, &T->mesh_out);
   prof_collect(T);
   return s;
+}
+
+int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {
+  memset(out, 0, sizeof(*out));
+  DevMesh m;
+  if (int s = extract_mesh_dev(T, iso, eps, &m)) return s;
+  return mesh_to_malloc(m, T->stream, out);
+}
+
+// two-phase extraction: the mesh stays on the device until the caller has
+// allocated its arrays, then one D2H per array straight into them
+int extract_mesh_begin(Table* T, double iso, double eps, int64_t* nv, int64_t* nt) {
+  DevMesh m;
+  T->mesh_nv = -1;
+  if (int s = extract_mesh_dev(T, iso, eps, &m)) return s;
+  if (m.nv && m.base != (char*)T->mesh_out.p) {
+    set_error("extract_mesh_begin: mesh not in the table buffer");
+    return kCudaError;
+  }
+  T->mesh_nv = m.nv;
+  T->mesh_nt = m.nt;
+  *nv = m.nv;
+  *nt = m.nt;
+  return kOk;
+}
+
+int extract_mesh_read(Table* T, double* v, double* n, double* c, int64_t* tri) {
+  if (T->mesh_nv < 0) {
+    set_error("extract_mesh_read: no extracted mesh (call extract_mesh_begin first)");
+    return kValueError;
+  }
+  DevMesh m;
+  m.base = (char*)T->mesh_out.p;
+  m.nv = T->mesh_nv;
+  m.nt = T->mesh_nt;
+  T->mesh_nv = -1;
+  return mesh_to_host(m, T->stream, v, n, c, tri);
 }
 
 int collapse_vertices(const double* v, const double* n, const double* c, int64_t nv,
@@ -991,7 +1090,9 @@ int collapse_vertices(const double* v, const double* n, const double* c, int64_t
   MCK(cudaMemcpy(dn, n, nv * 24, cudaMemcpyHostToDevice));
   MCK(cudaMemcpy(dc, c, nv * 24, cudaMemcpyHostToDevice));
   if (nt) MCK(cudaMemcpy(dt, tri, nt * 24, cudaMemcpyHostToDevice));
-  return collapse_device(S, dv, dn, dc, (uint64_t)nv, dt, (uint64_t)nt, eps, 0, out);
+  DevMesh m;
+  if (int s = collapse_device(S, dv, dn, dc, (uint64_t)nv, dt, (uint64_t)nt, eps, 0, &m, nullptr)) return s;
+  return mesh_to_malloc(m, 0, out);
 }
 
 void mesh_free(MeshOut* m) {

@@ -75,9 +75,17 @@ def extract_mesh(table: HashTable, iso: float = 0.0, collapse_epsilon=None) -> M
     eps = -1.0 if collapse_epsilon is None else float(collapse_epsilon)
     if collapse_epsilon is not None and eps < 0:
         raise ValueError("epsilon must be non-negative")
-    m = N.MeshC()
-    N.check(N.lib().tsdf_extract_mesh(table._h, float(iso), eps, C.byref(m)), "extract_mesh")
-    return _mesh_from_c(m)
+    nv, nt = C.c_int64(), C.c_int64()
+    L = N.lib()
+    N.check(L.tsdf_extract_mesh_begin(table._h, float(iso), eps, C.byref(nv), C.byref(nt)), "extract_mesh")
+    nv, nt = int(nv.value), int(nt.value)
+    if nv == 0 and nt == 0:
+        return Mesh.empty()
+    v, n, c = (np.empty((nv, 3), dtype=np.float64) for _ in range(3))
+    tri = np.empty((nt, 3), dtype=np.int64)
+    N.check(L.tsdf_extract_mesh_read(table._h, v.ctypes.data, n.ctypes.data, c.ctypes.data,
+                                     tri.ctypes.data), "extract_mesh")
+    return Mesh(vertices=v, normals=n, colors=c, triangles=tri)
 
 
 def collapse_vertices(mesh: Mesh, epsilon: float) -> Mesh:
