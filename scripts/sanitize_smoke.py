@@ -1,7 +1,8 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
 synccheck): depth window with merges (3 levels), the ray-sharded walk/keys
 split, a LiDAR scan, the capacity tier (evict / import / key pass), and mesh
-extraction -- every kernel family of the library, at sizes the sanitizer
+extraction, u16 depth, the NN metrics and the quadtree -- every kernel
+family of the library, at sizes the sanitizer
 finishes in minutes.
 
     compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
@@ -42,6 +43,18 @@ def main():
     pts = P.synth.lidar_frames(1, 16, 128)[0]
     tl = P.HashTable(1000003, 10, 7, 1.6, (40000, 1000))
     print("lidar", P.integrate_pointcloud(tl, pts, 0.8).observations)
+    # raw uint16 depth scaled on the device
+    raw = [P.DepthFrame(np.clip(np.round(np.nan_to_num(f.depth.astype(np.float64)) * 5000), 0, 65535)
+                        .astype(np.uint16), f.intrinsics, f.pose, color=f.color, depth_scale=5000.0)
+           for f in frames[:3]]
+    tu = P.HashTable(100003, 10, 7, 0.08, (20000, 10000))
+    print("u16", sum(s.voxels_updated for s in P.integrate_depth_batch(tu, raw, 0.03)))
+    # nearest-neighbour metrics and the quadtree / splat seeding
+    from paper_2511_21459_b200.metrics import eval_reconstruction
+    ref = np.random.default_rng(0).uniform(-2, 2, (5000, 3))
+    print("metrics", round(eval_reconstruction(m, ref, 0.1, samples_per_m2=2000)["fscore"], 4))
+    leaves = P.build_quadtree(np.asarray(frames[0].color, dtype=np.float64) / 255.0, 1e-5, 1)
+    print("quadtree", len(leaves), len(P.seed_splats(leaves, frames[0])))
     if "--no-engine" in sys.argv:
         return
     # capacity tier
