@@ -1,4 +1,4 @@
-for v in F H F H; do
+for v in ${VARIANTS:-F H F H}; do
   cp scripts/ab/fusion_$v.cu paper_2511_21459_b200/csrc/fusion.cu
   (cd paper_2511_21459_b200/csrc && make -s -j8 > /dev/null 2>&1)
   python - <<'P' > gpurun_out/walkonly_$v.txt 2>&1
