@@ -57,7 +57,7 @@ struct Table {
   // depth batches overlap frame k+1's allocation (walk stream) with frame
   // k's voxel update (main stream): per-parity copies of the frame scratch
   // that both sides read
-  Buf in0b, in1b, drayb, flagsb, pyrb, touchedb;
+  Buf in0b, in1b, drayb, flagsb, pyrb, touchedb, endsb;
   cudaStream_t walk_stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // H2D of host frames, ahead of the walk stream
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
