@@ -545,3 +545,23 @@ def test_sharded_extraction_equals_single_gpu(world):
         for x, y in ((a.vertices, b.vertices), (a.normals, b.normals), (a.colors, b.colors),
                      (a.triangles, b.triangles)):
             assert np.array_equal(x, y)
+
+
+def test_coordinates_beyond_the_packed_key_range_fail_cleanly():
+    """Block coordinates are packed 21 bits per axis (+-2^20 blocks, +-84 km
+    at 8 cm blocks); a measurement beyond that is a ValueError and leaves
+    the table as it was (the reference's int64 keys have no such limit,
+    DESIGN.md §3)."""
+    import paper_2511_21459_b200 as P
+    t = P.HashTable(100003, 10, 7, 0.08, (20000, 1000))
+    near = P.PointCloudFrame(points=np.array([[0.5, 0.1, 0.2], [1.0, -0.4, 0.3]]), pose=P.SensorPose.identity())
+    P.integrate_pointcloud(t, near, 0.04)
+    before = PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": t})()))
+    far = P.PointCloudFrame(points=np.array([[0.5, 0.1, 0.2], [9.0e4, 0.0, 0.0]]), pose=P.SensorPose.identity())
+    with pytest.raises(ValueError, match="21-bit"):
+        P.integrate_pointcloud(t, far, 0.04)
+    assert PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": t})())) == before
+    frame = _frame(P, np.full((8, 8), 1.0), pose=P.SensorPose(np.eye(3), [9.0e4, 0.0, 0.0]))
+    with pytest.raises(ValueError, match="21-bit"):
+        P.integrate_depth(t, frame, 0.04)
+    assert PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": t})())) == before
