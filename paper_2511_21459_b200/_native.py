@@ -158,7 +158,12 @@ def as_buffer(arr, allowed):
     """(pointer, dtype code, mem kind, keepalive) for a numpy array or a CUDA
     array (anything exposing __cuda_array_interface__, e.g. a torch tensor)."""
     codes = _CODES
-    if type(arr).__module__ == "torch" and arr.is_cuda:
+    if type(arr) is np.ndarray:
+        # fast path for the common case: a contiguous host array of a kernel dtype
+        code = codes.get(arr.dtype)
+        if code is not None and code in allowed and arr.flags.c_contiguous:
+            return arr.__array_interface__["data"][0], code, MEM_HOST, arr
+    elif type(arr).__module__ == "torch" and arr.is_cuda:
         # fast path: a torch tensor's __cuda_array_interface__ is rebuilt on
         # every access, which costs more than a frame's enqueue
         code = _TORCH_CODES.get(str(arr.dtype))
