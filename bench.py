@@ -522,11 +522,12 @@ def run_reference(args, wl):
     wall = max(r[2] for r in res) - min(r[1] for r in res)
     v = pts / wall / 1e6
     return {"impl": "reference", "metric": METRIC[args.workload],
-            "value": round(v, 4), "unit": "Mpoints/s", "n_gpus": 1, "steps": args.steps,
+            "value": round(v, 4), "unit": "Mpoints/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic ray-cast scene, deterministic)",
             "config": {"workload": wl["name"], "frames_per_step": 1, "replicas": n,
+                       "hardware": "host CPU only (n_gpus echoes the launch; no GPU is used)",
                        "note": "reference arm = the oracle port of the reference algorithm (the "
                                "reference is serial NumPy; same arithmetic, serial C) on every "
                                "usable host core: independent replicas of the frame stream"},
