@@ -447,13 +447,14 @@ def run_b200(args, wl, rank, world, dist, torch):
     return out
 
 
-def run_oracle_frames(wl, frames):
-    """The oracle port on the host (cpu_baseline / reference arm)."""
+def run_oracle_frames(wl, frames, keep=None):
+    """The oracle port on the host (cpu_baseline / reference arm); with a
+    dict `keep`, the oracle table and per-frame stats are left in it."""
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle.oracle import OracleTable
     # heaps sized for the bounded sample (calloc'd pages are only committed on touch)
     t = OracleTable(wl["n_hash"], 10, 7, wl["edge"], (600_000, 40_000, 10_000)[:len(wl["caps"])])
-    pts, secs = 0, []
+    pts, secs, stats = 0, [], []
     for d, c, pose, intr in frames:
         t0 = time.perf_counter()
         if wl["kind"] == "depth":
@@ -464,12 +465,43 @@ def run_oracle_frames(wl, frames):
             st = t.integrate_points(d.astype(np.float64), pose.rotation, pose.translation, wl["tau"])
         secs.append(time.perf_counter() - t0)
         pts += st["measurements"]
+        stats.append(st)
+    if keep is not None:
+        keep.update(table=t, stats=stats)
     return pts, secs
 
 
-def cpu_baseline(wl, n_frames=2):
+def parity_check(wl, frames, otable, ostats):
+    """the measured binary reproduces the reference algorithm on
+    the first frames of the measured workload -- per-frame counters equal and
+    the full table state (every level's keys, TSDF, weight, variance, colour)
+    bit-identical, compared as sha256 digests."""
+    import paper_2511_21459_b200 as P
+    import parity_utils as PU
+    t = make_table(P, wl)
+    gstats = []
+    for d, c, pose, intr in frames:
+        if wl["kind"] == "depth":
+            s = P.integrate_depth(t, P.DepthFrame(d, intr, pose, color=c), wl["tau"])
+        else:
+            s = P.integrate_pointcloud(t, P.PointCloudFrame(points=d, pose=pose), wl["tau"])
+        gstats.append({k: getattr(s, k) for k in PU.STAT_KEYS})
+    gstate = {l: tuple(t.export_level(l)[i] for i in (0, 2, 3, 4, 5)) for l in range(t.num_levels)}
+    ostate = {l: otable.block_arrays(l) for l in range(otable.num_levels)}
+    out = {"frames": len(frames),
+           "stats_equal": gstats == [{k: o[k] for k in PU.STAT_KEYS} for o in ostats],
+           "state_bit_identical": PU.state_digest(gstate) == PU.state_digest(ostate),
+           "blocks": [int(len(v[0])) for _, v in sorted(gstate.items())]}
+    t.close()
+    return out
+
+
+def cpu_baseline(wl, n_frames=2, parity=None):
     frames = make_frames(wl, n_frames)
-    pts, secs = run_oracle_frames(wl, frames)
+    keep = {}
+    pts, secs = run_oracle_frames(wl, frames, keep)
+    if parity is not None:
+        parity.update(parity_check(wl, frames, keep["table"], keep["stats"]))
     return {"value": round(pts / sum(secs) / 1e6, 4), "unit": "Mpoints/s", "cores": 1,
             "kind": "port",
             "sample": f"first {n_frames} frames of the same workload through the C oracle "
@@ -567,7 +599,9 @@ def main():
     out = run_b200(args, wl, rank, world, dist, torch)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(wl)
+            parity = {}
+            out["cpu_baseline"] = cpu_baseline(wl, parity=parity)
+            out["parity"] = parity
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
