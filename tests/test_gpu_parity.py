@@ -565,3 +565,23 @@ def test_coordinates_beyond_the_packed_key_range_fail_cleanly():
     with pytest.raises(ValueError, match="21-bit"):
         P.integrate_depth(t, frame, 0.04)
     assert PU.state_digest(PU.GpuBackend.state(type("x", (), {"t": t})())) == before
+
+
+@pytest.mark.parametrize("weight_cap,color", [(3.0, False), (2.5, True)])
+def test_lidar_weight_cap_hot_segments_vs_oracle(weight_cap, color):
+    """A dense scan (hot segments of > 1024 rays near the sensor take the
+    ray-parallel path) with an integral and a non-integral weight cap, with
+    and without colour: every compile-time variant of the hot apply against
+    the oracle (integrate.py:113-116)."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    scan = synth.lidar_frames(1, 96, 1536)[0]
+    if color:
+        scan.colors = np.random.default_rng(7).integers(0, 256, (len(scan.points), 3)).astype(np.uint8)
+    g = PU.GpuBackend(2000003, 1.6, (300000, 20000))
+    o = PU.OracleBackend(2000003, 1.6, (300000, 20000))
+    for _ in range(2):  # twice: the cap binds on the second pass
+        assert g.points(scan, 0.8, weight_cap=weight_cap) == o.points(scan, 0.8, weight_cap=weight_cap)
+    assert_states_match(g.state(), o.state())
+    w = g.state()[0][2]
+    assert w.max() == weight_cap
