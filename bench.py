@@ -64,6 +64,11 @@ METRIC = {"room": "integrated Mpoints/s (640x480 RGB-D room, 3 levels)",
           "room1024": "integrated Mpoints/s (1024x768 RGB-D room, 3 levels)",
           "lidar": "integrated Mpoints/s (128-beam LiDAR)"}
 FRAMES_PER_STEP = int(os.environ.get("TSDF_BENCH_WINDOW", "10"))  # = merge cadence
+# in-process parity sample per workload: (frames, merge cadence).  Room: two
+# full merge windows (20 frames, 2 passes at 3 levels); LiDAR: 4 scans with a
+# merge pass every 2 (the oracle needs ~12 s per 128x2048 scan)
+PARITY = {"room": (20, 10), "room1024": (20, 10), "room_fixed5mm": (20, 10), "lidar": (4, 2)}
+LIDAR_STEPS = 5  # timed windows of the N=1 LiDAR sub-run (10 scans each)
 S_IN = {"depth": 7, "lidar": 12}  # algorithmic input bytes per measurement
 
 
@@ -170,6 +175,22 @@ def make_frames(wl, n, start=0):
     return out
 
 
+def _gen_one(a):
+    name, i = a
+    return make_frames(WORKLOADS[name], 1, i)[0]
+
+
+def gen_frames(name, n, start=0):
+    """make_frames on a process pool (rendering is per-frame independent)."""
+    import multiprocessing as mp
+    procs = max(1, min(n, 32, (os.cpu_count() or 1) - 2))
+    if n <= 4 or procs == 1:
+        return make_frames(WORKLOADS[name], n, start)
+    with mp.get_context("fork").Pool(procs) as pool:
+        return pool.map(_gen_one, [(name, i) for i in range(start, start + n)],
+                        chunksize=max(1, n // (4 * procs)))
+
+
 def n_meas(fr):
     d = fr[0]
     return int(np.count_nonzero(np.isfinite(d) & (d > 0))) if d.ndim == 2 else int(len(d))
@@ -246,19 +267,22 @@ def kernel_bytes(stats_list, wl):
 KERNEL_ROLE = {"k_depth_update": "update", "k_lidar_update": "update", "k_dda_walk": "alloc"}
 
 
-def run_b200(args, wl, rank, world, dist, torch):
+def run_b200(name, W, K, rank, world, dist, torch, frames=None):
+    """The B200 arm on workload `name`: W warm-up windows, K timed windows
+    (inputs resident in HBM), K profiled windows, then the e2e run."""
     import paper_2511_21459_b200 as P
+    wl = WORKLOADS[name]
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
     shard = (rank, world) if world > 1 else None
     if world > 1:
         _MULTI.update(dist=dist, torch=torch, device=dev)
-    W, K = args.warmup, args.steps
     nfr = FRAMES_PER_STEP * (W + 2 * K)  # warm-up, timed, then profiled windows
-    t0 = time.time()
-    frames = make_frames(wl, nfr)
-    log(f"[bench] generated {nfr} frames in {time.time() - t0:.1f}s")
+    if frames is None or len(frames) < nfr:
+        t0 = time.time()
+        frames = gen_frames(name, nfr)
+        log(f"[bench] generated {nfr} {name} frames in {time.time() - t0:.1f}s")
     # device-resident inputs
     dframes = []
     for d, c, _, _ in frames:
@@ -394,27 +418,36 @@ def run_b200(args, wl, rank, world, dist, torch):
     top_bytes = Bp[role] if role in Bp else Bp["path"]
     achieved = (top_bytes / top_n) / ((top_ms / top_n) * 1e-3) / 1e9 if top_ms > 0 else 0.0
     path_gbs = B["path"] / (dev_ms * 1e-3) / 1e9
-    traffic, ncu = None, {}
-    prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
-        try:
-            ncu = json.loads(prof.read_text())
-            traffic = ncu.get("traffic_per_launch", {}).get(top_name)
-        except Exception:
-            traffic, ncu = None, {}
+    ncu, ncu_note = ncu_profile()
+    traffic = ncu.get("kernels", {}).get(top_name, {}).get("dram_bytes")
+    clocks = sampler.summary()
     # the binding resource of the walk is instruction issue (FP64 DDA
-    # steps), not HBM: report its work rate beside the HBM roofline
+    # steps), not HBM: its issue roofline = the warp instructions one launch
+    # executes (ncu, same build) over the SM issue capacity (148 SMs x 4
+    # schedulers x 1 warp-instruction per cycle at the sampled clock),
+    # against the live launch time
     secondary = None
-    if "k_dda_walk" in ktimes and work.get("dda_steps"):
-        w_ms, w_n = ktimes["k_dda_walk"]
+    walk = "k_dda_walk"
+    if walk in ktimes and work.get("dda_steps"):
+        w_ms, w_n = ktimes[walk]
         steps = work["dda_steps"] / max(w_n, 1)
-        secondary = {"bound": "issue (FP64 DDA steps)", "kernel": "k_dda_walk",
-                     "dda_steps_per_launch": round(steps),
-                     "ms_per_launch": round(w_ms / max(w_n, 1), 4),
-                     "gsteps_per_s": round(steps / (w_ms / max(w_n, 1) * 1e-3) / 1e9, 3),
-                     "ncu_issue_active_frac": ncu.get("issue_active_frac", {}).get("k_dda_walk")}
+        ms_launch = w_ms / max(w_n, 1)
+        kw = ncu.get("kernels", {}).get(walk, {})
+        secondary = {"bound": "issue (FP64 DDA steps)", "kernel": walk,
+                     "dda_steps_per_launch": round(steps), "ms_per_launch": round(ms_launch, 4),
+                     "gsteps_per_s": round(steps / (ms_launch * 1e-3) / 1e9, 3)}
+        if kw.get("warp_inst") and clocks.get("sm_mhz"):
+            sms = ncu.get("sms", 148)
+            # ncu counts one launch (one frame of the capture driver, whose
+            # DDA steps it recorded); scale to this run's steps per launch
+            inst_per_step = kw["warp_inst"] / max(kw.get("dda_steps", steps), 1)
+            floor_ms = inst_per_step * steps / (sms * 4 * clocks["sm_mhz"] * 1e6) * 1e3
+            secondary.update({"warp_inst_per_step": round(inst_per_step, 3),
+                              "issue_floor_ms": round(floor_ms, 4),
+                              "issue_frac": round(floor_ms / ms_launch, 4),
+                              "ncu_issue_active_frac": kw.get("issue_active")})
     out = {
-        "metric": METRIC[args.workload],
+        "metric": METRIC[name],
         "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(dev_ms / K, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -442,79 +475,140 @@ def run_b200(args, wl, rank, world, dist, torch):
         "kernels_ms": {k: [round(v[0], 3), v[1]] for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])},
         "gpu_launches": int(launches),
         "extract": extract,
-        "clocks": sampler.summary(),
+        "clocks": clocks,
     }
+    out["roofline"]["ncu"] = ncu_note
     return out
 
 
-def run_oracle_frames(wl, frames, keep=None):
-    """The oracle port on the host (cpu_baseline / reference arm); with a
-    dict `keep`, the oracle table and per-frame stats are left in it."""
-    sys.path.insert(0, str(ROOT / "tests"))
+def ncu_profile():
+    """profiles/ncu_summary.json if it was captured on this exact build
+    (source digest of csrc + the ABI header); otherwise nothing, and the
+    roofline says why (a stale capture would misreport traffic)."""
+    from paper_2511_21459_b200._native import source_digest
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if not prof.exists():
+        return {}, "no ncu summary"
+    try:
+        d = json.loads(prof.read_text())
+    except Exception as e:
+        return {}, f"unreadable ncu summary: {e}"
+    want = source_digest()
+    if d.get("src_sha") != want:
+        return {}, f"ncu summary is from build {d.get('src_sha')}, this build is {want}: dropped"
+    return d, f"ncu --set full on this build ({want}): {d.get('source', '')}"
+
+
+def _oracle_table(wl):
     from oracle.oracle import OracleTable
-    # heaps sized for the bounded sample (calloc'd pages are only committed on touch)
-    t = OracleTable(wl["n_hash"], 10, 7, wl["edge"], (600_000, 40_000, 10_000)[:len(wl["caps"])])
-    pts, secs, stats = 0, [], []
-    for d, c, pose, intr in frames:
-        t0 = time.perf_counter()
-        if wl["kind"] == "depth":
-            st = t.integrate_depth(d.astype(np.float64), [intr.fx, intr.fy, intr.cx, intr.cy],
-                                   pose.rotation, pose.translation, wl["tau"],
-                                   color=c.astype(np.float64) / 255.0)
-        else:
-            st = t.integrate_points(d.astype(np.float64), pose.rotation, pose.translation, wl["tau"])
-        secs.append(time.perf_counter() - t0)
-        pts += st["measurements"]
-        stats.append(st)
-    if keep is not None:
-        keep.update(table=t, stats=stats)
-    return pts, secs
+    # the GPU table's capacities (calloc'd heaps: pages are committed on touch)
+    return OracleTable(wl["n_hash"], 10, 7, wl["edge"], wl["caps"])
 
 
-def parity_check(wl, frames, otable, ostats):
-    """the measured binary reproduces the reference algorithm on
-    the first frames of the measured workload -- per-frame counters equal and
-    the full table state (every level's keys, TSDF, weight, variance, colour)
-    bit-identical, compared as sha256 digests."""
-    import paper_2511_21459_b200 as P
+def oracle_frame(t, wl, fr):
+    d, c, pose, intr = fr
+    if wl["kind"] == "depth":
+        return t.integrate_depth(d.astype(np.float64), [intr.fx, intr.fy, intr.cx, intr.cy],
+                                 pose.rotation, pose.translation, wl["tau"],
+                                 color=None if c is None else c.astype(np.float64) / 255.0)
+    return t.integrate_points(d.astype(np.float64), pose.rotation, pose.translation, wl["tau"])
+
+
+def oracle_parity_job(name, q):
+    """Child process: the oracle (test infrastructure; the checker and the
+    CPU baseline, never the product) on the parity sample of `name` --
+    per-frame stats, merge passes every `cadence` frames (all levels), per-
+    frame host time, and the final state's digest."""
+    sys.path.insert(0, str(ROOT / "tests"))
     import parity_utils as PU
+    wl = WORKLOADS[name]
+    n, cadence = PARITY[name]
+    frames = make_frames(wl, n)
+    t = _oracle_table(wl)
+    stats, merges, secs, pts = [], [], [], []
+    for i, fr in enumerate(frames):
+        t0 = time.perf_counter()
+        st = oracle_frame(t, wl, fr)
+        if (i + 1) % cadence == 0:
+            merges.append(t.apply_merges(wl["sigma"], all_levels=True))
+        secs.append(time.perf_counter() - t0)
+        pts.append(st["measurements"])
+        stats.append({k: st[k] for k in PU.STAT_KEYS})
+    state = {l: t.block_arrays(l) for l in range(t.num_levels)}
+    q.put({"stats": stats, "merges": merges, "secs": secs, "pts": pts,
+           "digest": PU.state_digest(state), "keys": PU.keys_digest(state),
+           "blocks": [int(len(v[0])) for _, v in sorted(state.items())]})
+
+
+def gpu_parity(P, name, frames):
+    """The measured binary on the parity sample, through the same window
+    calls the timed region uses."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import parity_utils as PU
+    wl = WORKLOADS[name]
+    n, cadence = PARITY[name]
     t = make_table(P, wl)
-    gstats = []
-    for d, c, pose, intr in frames:
+    stats, merges = [], []
+    for w0 in range(0, n, cadence):
+        win = frames[w0:w0 + cadence]
         if wl["kind"] == "depth":
-            s = P.integrate_depth(t, P.DepthFrame(d, intr, pose, color=c), wl["tau"])
+            fs = [P.DepthFrame(depth=d, intrinsics=intr, pose=pose, color=c) for d, c, pose, intr in win]
+            st, ms = P.integrate_depth_window(t, fs, wl["tau"], wl["sigma"], all_levels=True)
         else:
-            s = P.integrate_pointcloud(t, P.PointCloudFrame(points=d, pose=pose), wl["tau"])
-        gstats.append({k: getattr(s, k) for k in PU.STAT_KEYS})
-    gstate = {l: tuple(t.export_level(l)[i] for i in (0, 2, 3, 4, 5)) for l in range(t.num_levels)}
-    ostate = {l: otable.block_arrays(l) for l in range(otable.num_levels)}
-    out = {"frames": len(frames),
-           "stats_equal": gstats == [{k: o[k] for k in PU.STAT_KEYS} for o in ostats],
-           "state_bit_identical": PU.state_digest(gstate) == PU.state_digest(ostate),
-           "blocks": [int(len(v[0])) for _, v in sorted(gstate.items())]}
+            st = [P.integrate_pointcloud(t, P.PointCloudFrame(points=d, pose=pose), wl["tau"])
+                  for d, _, pose, _ in win]
+            ms = P.apply_merges(t, wl["sigma"], all_levels=True)
+        stats += [{k: getattr(x, k) for k in PU.STAT_KEYS} for x in st]
+        merges.append({"candidates": ms.candidates, "merged": ms.merged})
+    state = {l: tuple(t.export_level(l)[i] for i in (0, 2, 3, 4, 5)) for l in range(t.num_levels)}
+    out = {"stats": stats, "merges": merges, "digest": PU.state_digest(state),
+           "keys": PU.keys_digest(state), "blocks": [int(len(v[0])) for _, v in sorted(state.items())]}
     t.close()
     return out
 
 
-def cpu_baseline(wl, n_frames=2, parity=None):
-    frames = make_frames(wl, n_frames)
-    keep = {}
-    pts, secs = run_oracle_frames(wl, frames, keep)
-    if parity is not None:
-        parity.update(parity_check(wl, frames, keep["table"], keep["stats"]))
-    return {"value": round(pts / sum(secs) / 1e6, 4), "unit": "Mpoints/s", "cores": 1,
-            "kind": "port",
-            "sample": f"first {n_frames} frames of the same workload through the C oracle "
-                      f"(oracle/tsdf_oracle.c, serial, -O2), {sum(secs):.1f} s"}
+def parity_and_baseline(name, g, o):
+    """the measured binary reproduces the reference algorithm
+    (the oracle) on the first frames of the measured workload, merges
+    included; the oracle's steady-state frames are the CPU baseline."""
+    n, cadence = PARITY[name]
+    parity = {"frames": n, "merge_cadence": cadence, "merge_passes": len(g["merges"]),
+              "levels": "all (labelled 3-level extension, oracle all_levels=True)",
+              "merged": int(sum(m["merged"] for m in g["merges"])),
+              "stats_equal": g["stats"] == o["stats"],
+              "merges_equal": g["merges"] == o["merges"],
+              "keys_bit_identical": g["keys"] == o["keys"],
+              "state_bit_identical": g["digest"] == o["digest"],
+              "blocks": g["blocks"], "oracle_blocks": o["blocks"],
+              "compared": "per-frame IntegrationStats, per-pass MergeStats, sha256 of every level's "
+                          "keys + TSDF + weight + variance + colour"}
+    # steady state: frames after the first (whose allocation is the whole
+    # visible map), merge passes included
+    secs, pts = sum(o["secs"][1:]), sum(o["pts"][1:])
+    base = {"value": round(pts / secs / 1e6, 4), "unit": "Mpoints/s", "cores": 1, "kind": "port",
+            "sample": f"frames 2..{n} of the parity sample (merge every {cadence}) through the C "
+                      f"oracle (oracle/tsdf_oracle.c, serial, -O2): {pts} points in {secs:.1f} s"}
+    return parity, base
 
 
 def _reference_worker(wl, frames, warmup, barrier, q):
-    """One replica of the reference arm: warm-up frames, then (after every
-    replica is ready) the timed frames into its own table."""
-    run_oracle_frames(wl, frames[:warmup])
+    """One replica of the reference arm: the frame stream into its own table
+    with a merge pass (all levels) after every FRAMES_PER_STEP-th frame, as
+    the measured B200 arm does; the first `warmup` frames are untimed."""
+    t = _oracle_table(wl)
+
+    def run(i0, i1):
+        pts = 0
+        for i in range(i0, i1):
+            pts += oracle_frame(t, wl, frames[i])["measurements"]
+            if (i + 1) % FRAMES_PER_STEP == 0:
+                t.apply_merges(wl["sigma"], all_levels=True)
+        return pts
+
+    run(0, warmup)
     barrier.wait()
     t0 = time.time()
-    pts, _ = run_oracle_frames(wl, frames[warmup:])
+    pts = run(warmup, len(frames))
     q.put((pts, t0, time.time()))
 
 
@@ -531,7 +625,7 @@ def reference_replicas(wl):
     return max(1, n)
 
 
-def run_reference(args, wl):
+def run_reference(args, name):
     """The reference arm: the reference algorithm (the oracle port; the
     reference is serial NumPy) on every host core it can use.  The path is
     serial per table, so the cores run independent replicas of the same
@@ -539,7 +633,8 @@ def run_reference(args, wl):
     all replicas' timed points / the wall time from the common start to the
     last replica's end."""
     import multiprocessing as mp
-    frames = make_frames(wl, args.warmup + args.steps)
+    wl = WORKLOADS[name]
+    frames = gen_frames(name, args.warmup + args.steps)
     n = reference_replicas(wl)
     ctx = mp.get_context("fork")
     barrier, q = ctx.Barrier(n), ctx.Queue()
@@ -553,21 +648,31 @@ def run_reference(args, wl):
     pts = sum(r[0] for r in res)
     wall = max(r[2] for r in res) - min(r[1] for r in res)
     v = pts / wall / 1e6
-    return {"impl": "reference", "metric": METRIC[args.workload],
+    return {"impl": "reference", "metric": METRIC[name],
             "value": round(v, 4), "unit": "Mpoints/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic ray-cast scene, deterministic)",
             "config": {"workload": wl["name"], "frames_per_step": 1, "replicas": n,
+                       "merge_passes": f"all levels, after every {FRAMES_PER_STEP}th frame of "
+                                       "the stream (as the B200 arm)",
                        "hardware": "host CPU only (n_gpus echoes the launch; no GPU is used)",
                        "note": "reference arm = the oracle port of the reference algorithm (the "
                                "reference is serial NumPy; same arithmetic, serial C) on every "
                                "usable host core: independent replicas of the frame stream"},
             "cpu_baseline": {"value": round(v, 4), "unit": "Mpoints/s", "cores": n, "kind": "port",
-                             "sample": f"{args.steps} timed frames after {args.warmup} warm-up, "
-                                       f"{n} replicas in parallel"},
+                             "sample": f"frames {args.warmup + 1}..{args.warmup + args.steps} "
+                                       f"of the stream (merges included) after {args.warmup} "
+                                       f"warm-up frames, {n} replicas in parallel"},
             "e2e": {"value": round(v, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def _sub_line(o):
+    """The keys of a workload's line kept in the N=1 line's sub-object."""
+    keep = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "config", "e2e",
+            "roofline", "kernels_ms", "gpu_launches", "clocks", "cpu_baseline", "parity")
+    return {k: o[k] for k in keep if k in o}
 
 
 def main():
@@ -577,31 +682,63 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="room", choices=list(WORKLOADS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true",
+                    help="skip the oracle parity check and CPU baseline")
+    ap.add_argument("--no-lidar", action="store_true",
+                    help="N=1 room runs: skip the LiDAR (config 3) sub-run")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path with ranks sharing one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    wl = WORKLOADS[args.workload]
+    name = args.workload
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args, wl)), flush=True)
+            print(json.dumps(run_reference(args, name)), flush=True)
         return
+    # BASELINE's metric is quoted on both north-star configs: an N=1 room
+    # run also measures the 128-beam LiDAR stream (config 3) as `lidar`
+    subs = ["lidar"] if world == 1 and name.startswith("room") and not args.no_lidar else []
+    check = world == 1 and not args.no_cpu_baseline
+    # the oracle runs (checker + CPU baseline) start first, in their own
+    # processes, before CUDA is initialised here
+    jobs = {}
+    if check:
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        for nm in [name] + subs:
+            q = ctx.Queue()
+            p = ctx.Process(target=oracle_parity_job, args=(nm, q), daemon=True)
+            p.start()
+            jobs[nm] = (p, q)
+    t0 = time.time()
+    frames = {nm: gen_frames(nm, FRAMES_PER_STEP * (args.warmup + 2 * (args.steps if nm == name
+                                                                         else min(args.steps, LIDAR_STEPS))))
+              for nm in [name] + subs}
+    log(f"[bench] generated frames for {list(frames)} in {time.time() - t0:.1f}s")
     import torch
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1))
         dist.init_process_group(args.dist_backend)
-    out = run_b200(args, wl, rank, world, dist, torch)
+    out = run_b200(name, args.warmup, args.steps, rank, world, dist, torch, frames[name])
+    for nm in subs:
+        out[nm] = _sub_line(run_b200(nm, args.warmup, min(args.steps, LIDAR_STEPS), rank, world,
+                                     dist, torch, frames[nm]))
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
-            parity = {}
-            out["cpu_baseline"] = cpu_baseline(wl, parity=parity)
-            out["parity"] = parity
+        if check:
+            import paper_2511_21459_b200 as P
+            for nm in [name] + subs:
+                n = PARITY[nm][0]
+                g = gpu_parity(P, nm, frames[nm][:n] if len(frames[nm]) >= n else make_frames(WORKLOADS[nm], n))
+                p, q = jobs[nm]
+                o = q.get()
+                p.join()
+                tgt = out if nm == name else out[nm]
+                tgt["parity"], tgt["cpu_baseline"] = parity_and_baseline(nm, g, o)
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()

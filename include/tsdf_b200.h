@@ -14,7 +14,10 @@
  * Ownership: the table owns all device memory; callers own input buffers
  * for the duration of a call.  `mem` says where input buffers live
  * (TSDF_MEM_HOST: pageable/pinned host memory, copied inside the call;
- * TSDF_MEM_DEVICE: device pointers, read in place).
+ * TSDF_MEM_DEVICE: device pointers, read in place on the table's stream:
+ * their contents must be complete when the call is made -- a buffer written
+ * by work on another stream, e.g. an NCCL collective on torch's current
+ * stream, needs that stream synchronised (or an event waited on) first).
  */
 #ifndef TSDF_B200_H
 #define TSDF_B200_H
@@ -297,6 +300,16 @@ int tsdf_profile_read(tsdf_table *t, int32_t reset, int32_t max_entries, char *n
 const char *tsdf_last_error(void);
 int64_t tsdf_kernel_launches(tsdf_table *t);
 int64_t tsdf_table_slots(tsdf_table *t);
+/* Block-index health.  Erased entries (remove, evict, capacity rollback)
+ * leave tombstones in the open-addressing index; inserts reuse them, and
+ * the index is rebuilt without them (tsdf_table_compact, run automatically
+ * before an inserting call once they pass a quarter of the slots).  The
+ * reference frees its chain entries on remove (hashgrid.py:253-275).
+ * out: [0] live entries, [1] tombstones, [2] longest probe sequence of a
+ * live key (1 = at its home slot), [3] rebuilds so far; *mean_probe = the
+ * average probe length of the live keys. */
+int tsdf_table_probe_stats(tsdf_table *t, int64_t *out, double *mean_probe);
+int tsdf_table_compact(tsdf_table *t);
 int tsdf_device_info(int32_t *sm_major, int32_t *sm_minor, int32_t *num_sms);
 
 #ifdef __cplusplus

@@ -52,6 +52,19 @@ def build(force: bool = False) -> Path:
     return LIB_PATH
 
 
+def source_digest() -> str:
+    """sha256 (16 hex) of the CUDA sources and the ABI header: identifies the
+    build a profile was captured on (there is no .git on the GPU box)."""
+    import hashlib
+    h = hashlib.sha256()
+    src = _PKG / "csrc"
+    for p in sorted(list(src.glob("*.cu")) + list(src.glob("*.cuh")) + list(src.glob("*.h"))
+                    + [src / "Makefile", _PKG.parent / "include" / "tsdf_b200.h"]):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()[:16]
+
+
 _ptr = C.c_void_p
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
@@ -120,6 +133,8 @@ def lib():
     L.tsdf_table_slots.restype = i64
     L.tsdf_table_slots.argtypes = [_ptr]
     L.tsdf_device_info.argtypes = [C.POINTER(i32)] * 3
+    L.tsdf_table_probe_stats.argtypes = [_ptr, _i64p, C.POINTER(dbl)]
+    L.tsdf_table_compact.argtypes = [_ptr]
     L.tsdf_dda_blocks.argtypes = [_ptr, _ptr, i64, dbl, i32, C.POINTER(C.POINTER(i64)),
                                   C.POINTER(C.POINTER(i64)), C.POINTER(i64)]
     L.tsdf_merge_candidates.argtypes = [_ptr, dbl, dbl, dbl, C.POINTER(C.POINTER(i64)),

@@ -284,6 +284,23 @@ int tsdf_write_block(tsdf_table* t, const int64_t* coord, const double* tsdf,
   return write_block(T_(t), coord, tsdf, weight, s2, color);
 }
 
+int tsdf_table_probe_stats(tsdf_table* t, int64_t* out, double* mean_probe) {
+  NEED(t);
+  ProbeStats p;
+  if (int s = probe_stats(T_(t), &p)) return s;
+  out[0] = p.live;
+  out[1] = p.tombstones;
+  out[2] = p.max_probe;
+  out[3] = p.rehashes;
+  if (mean_probe) *mean_probe = p.mean_probe;
+  return TSDF_OK;
+}
+
+int tsdf_table_compact(tsdf_table* t) {
+  NEED(t);
+  return rehash_table(T_(t));
+}
+
 int tsdf_live_count(tsdf_table* t, int32_t level, int64_t* n) {
   NEED(t);
   return live_count(T_(t), level, n);

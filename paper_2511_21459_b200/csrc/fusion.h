@@ -42,6 +42,10 @@ struct Table {
   bool own_stream = false;
   Counters* dcnt = nullptr;  // device
   Counters* hcnt = nullptr;  // pinned host mirror
+  // pinned copy of DevTable::n_tomb, refreshed at the end of every call that
+  // synchronises; maintain_table() rebuilds the index once it passes slots/4
+  unsigned long long* htomb = nullptr;
+  uint64_t rehashes = 0;
   uint32_t call_id = 0;
   double depth_scale = 1.0;  // raw u16 depth units per metre (tsdf_table_set_depth_scale)
   Buf mesh_out;                   // the last extract_mesh_begin result (device)
@@ -121,6 +125,15 @@ int table_create(int64_t n_hash, int32_t bucket, int32_t overflow, double block_
                  int32_t n_levels, const int64_t* caps, void* stream, Table** out);
 int table_destroy(Table* t);
 int table_reset(Table* t);
+// rebuild the block index without tombstones (slot ids change; callable only
+// between calls); maintain_table() does it when tombstones pass slots / 4
+int rehash_table(Table* T);
+int maintain_table(Table* T);
+struct ProbeStats {
+  int64_t live, tombstones, max_probe, rehashes;
+  double mean_probe;
+};
+int probe_stats(Table* T, ProbeStats* out);
 
 struct DepthArgs {
   const void* depth;

@@ -79,6 +79,9 @@ struct DevTable {
   uint32_t* dirty;       // per slot flag
   uint32_t* dirty_list;  // slots, in first-dirtied order
   unsigned long long* n_dirty;
+  // tombstones in keys[] (erased entries): reused by inserts, and the host
+  // rebuilds the table once they pass a quarter of the slots (rehash_table)
+  unsigned long long* n_tomb;
   DevHeap heap[kMaxLevels];
 };
 
@@ -122,7 +125,7 @@ struct MergeDev {
   unsigned long long n_list;
   unsigned long long n_dirty;  // dirty-list length at the pass (snapshot)
   uint32_t skip;
-  uint32_t pad;
+  uint32_t pad;  // k_merge_apply: 1 = a merged weight was rounded to binary32
 };
 
 __host__ __device__ inline uint64_t pack_key(int64_t x, int64_t y, int64_t z) {
@@ -184,28 +187,47 @@ __device__ inline int64_t table_find(const DevTable& t, uint64_t key) {
   return -1;
 }
 
-// lock-free find-or-insert of a key (64-bit atomicCAS, linear probing).
+// Lock-free find-or-insert of a key (64-bit atomicCAS, linear probing).
 // Returns slot (or -1 if the table is full); *inserted set when this
-// thread created the entry.
+// thread created the entry.  The key goes to the first tombstone on its
+// probe path, but only after the scan has reached an EMPTY slot without
+// meeting the key (so a key is never live twice); with no tombstone on the
+// path it takes that EMPTY slot.  A lost CAS race rescans from home.
+// Erasure never runs concurrently with inserts (separate kernels).
 __device__ inline int64_t table_find_or_insert(const DevTable& t, uint64_t key, bool* inserted) {
   *inserted = false;
-  uint64_t i = mix64(key) & t.mask;
-  for (uint64_t probe = 0; probe <= t.mask; probe++) {
-    uint64_t k = __ldcg(&t.keys[i]);
-    if (k == key) return (int64_t)i;
-    if (k == kEmptyKey) {
-      unsigned long long old =
-          atomicCAS((unsigned long long*)&t.keys[i], (unsigned long long)kEmptyKey,
-                    (unsigned long long)key);
-      if (old == kEmptyKey) {
-        *inserted = true;
-        return (int64_t)i;
-      }
-      if (old == key) return (int64_t)i;
+  const uint64_t home = mix64(key) & t.mask;
+  for (;;) {
+    uint64_t i = home, probe = 0;
+    int64_t tomb = -1;
+    for (; probe <= t.mask; probe++) {
+      const uint64_t k = __ldcg(&t.keys[i]);
+      if (k == key) return (int64_t)i;
+      if (k == kEmptyKey) break;
+      if (k == kTombKey && tomb < 0) tomb = (int64_t)i;
+      i = (i + 1) & t.mask;
     }
-    i = (i + 1) & t.mask;
+    if (probe > t.mask && tomb < 0) return -1;  // no EMPTY and no tombstone left
+    const uint64_t at = tomb >= 0 ? (uint64_t)tomb : i;
+    const unsigned long long expect = tomb >= 0 ? kTombKey : kEmptyKey;
+    const unsigned long long old =
+        atomicCAS((unsigned long long*)&t.keys[at], expect, (unsigned long long)key);
+    if (old == expect) {
+      if (tomb >= 0) atomicAdd(t.n_tomb, ~0ull);  // one tombstone fewer
+      *inserted = true;
+      return (int64_t)at;
+    }
+    if (old == key) return (int64_t)at;
   }
-  return -1;
+}
+
+// erase a live entry (remove, evict, merge-free never erases: re-home keeps
+// the key): the slot becomes a tombstone that later inserts reuse
+__device__ inline void table_erase(const DevTable& t, uint64_t slot) {
+  t.vals[slot] = kPending;
+  t.stamp[slot] = 0;
+  t.keys[slot] = kTombKey;
+  atomicAdd(t.n_tomb, 1ull);
 }
 
 // warp-aggregated append to a device list: one atomic per warp

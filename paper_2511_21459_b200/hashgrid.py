@@ -217,6 +217,21 @@ class HashTable:
         """Device hash-table slots (the bound on distinct blocks one call can touch)."""
         return int(N.lib().tsdf_table_slots(self._h))
 
+    def probe_stats(self) -> dict:
+        """Block-index health: live entries, tombstones left by erased
+        blocks, the longest / mean probe sequence of a live key and the
+        number of tombstone rebuilds so far."""
+        out = np.zeros(4, np.int64)
+        mean = C.c_double()
+        N.check(N.lib().tsdf_table_probe_stats(self._h, out, C.byref(mean)), "probe_stats")
+        return {"live": int(out[0]), "tombstones": int(out[1]), "max_probe": int(out[2]),
+                "rehashes": int(out[3]), "mean_probe": float(mean.value)}
+
+    def compact(self) -> None:
+        """Rebuild the block index without tombstones (done automatically
+        once they pass a quarter of the slots)."""
+        N.check(N.lib().tsdf_table_compact(self._h), "compact")
+
     @property
     def kernel_launches(self) -> int:
         return int(N.lib().tsdf_kernel_launches(self._h))

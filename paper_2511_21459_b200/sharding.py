@@ -122,6 +122,17 @@ def _bytes_of(a, torch, device):
     return torch.from_numpy(h.reshape(-1).view(np.uint8)).to(device), h.dtype.str, h.shape
 
 
+def stream_ready(t, torch):
+    """Make a tensor a collective just wrote safe to hand to the library.
+    NCCL collectives only order torch's current stream; the library runs on
+    its own stream, so the host waits for torch's stream before passing the
+    buffer on (tsdf_b200.h: TSDF_MEM_DEVICE buffers must be ready at the
+    call)."""
+    if t is not None and getattr(t, "is_cuda", False):
+        torch.cuda.current_stream(t.device).synchronize()
+    return t
+
+
 def _bcast_array(a, rank, dist, torch, group, device):
     """Broadcast one array from rank 0 bit-for-bit in its own element type
     (f64 / f32 / u8 / u16): a header of (type, rank, shape), then the bytes."""
@@ -141,7 +152,7 @@ def _bcast_array(a, rank, dist, torch, group, device):
                           device=device)
     dist.broadcast(raw, 0, group=group)
     if raw.is_cuda:
-        return _DeviceView(raw, typestr, shape)
+        return _DeviceView(stream_ready(raw, torch), typestr, shape)
     return raw.numpy().view(np.dtype(typestr)).reshape(shape)
 
 
@@ -210,7 +221,7 @@ def exchange_keys(buckets, counts, dist, torch, group=None, device=None):
         send = send.cpu()
     recv = torch.empty(sum(rc), dtype=send.dtype, device=send.device)
     dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc, group=group)
-    return recv.to(out_dev)
+    return stream_ready(recv.to(out_dev), torch)
 
 
 def integrate_depth_raysharded(table, frame, tau, dist, torch, group=None, device=None,
