@@ -141,15 +141,16 @@ def render_depth(scene: Scene, pose: SensorPose, intr: Intrinsics, width: int, h
 
 
 def render_frames(scene_name: str, frames: int, width: int, height: int,
-                  depth_dtype=np.float64, color_dtype=np.float64) -> list:
+                  depth_dtype=np.float64, color_dtype=np.float64, sweep: int | None = None) -> list:
     """Depth frames along the scene's trajectory.  float32 depth / uint8 colour
     give the compact 7 B/px sensor format (values quantised before use, so
-    every consumer sees the same inputs)."""
+    every consumer sees the same inputs).  ``sweep``: the trajectory's length
+    when only its first ``frames`` poses are rendered (default: frames)."""
     scene = make_scene(scene_name)
     intr = default_intrinsics(scene_name, width, height)
     base = scene if scene_name != "large_room" else Scene("room", scene.spheres, None, scene.room)
     out = []
-    for i, pose in enumerate(trajectory(base, frames)):
+    for i, pose in enumerate(trajectory(base, sweep or frames)[:frames]):
         d, c = render_depth(scene, pose, intr, width, height)
         d = d.astype(depth_dtype)
         c = (np.round(c * 255.0).astype(np.uint8) if color_dtype == np.uint8 else c.astype(color_dtype))

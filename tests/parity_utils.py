@@ -254,11 +254,11 @@ BACKENDS = {"reference": RefBackend, "oracle": OracleBackend, "gpu": GpuBackend}
 
 def run_depth_scenario(backend, scene, frames, width, height, edge, tau, caps, n_hash,
                        sigma=None, cadence=10, all_levels=False, color=True, weight_cap=0.0,
-                       depth_dtype=np.float64, color_dtype=np.float64):
+                       depth_dtype=np.float64, color_dtype=np.float64, sweep=None):
     from paper_2511_21459_b200 import synth
     b = BACKENDS[backend](n_hash, edge, caps)
     seq = synth.render_frames(scene, frames, width, height, depth_dtype=depth_dtype,
-                              color_dtype=color_dtype)
+                              color_dtype=color_dtype, sweep=sweep)
     stats, merges = [], []
     for i, f in enumerate(seq):
         if not color:
@@ -287,3 +287,50 @@ def run_lidar_scenario(backend, scans, beams, columns, edge, tau, caps, n_hash, 
 
 def level_summary(state):
     return {int(l): int(len(v[0])) for l, v in state.items()}
+
+
+# ---------------------------------------------------------------------------
+# full-scale scenarios (tests/golden/golden_full.json, scripts/make_golden_full.py)
+# ---------------------------------------------------------------------------
+
+FULL_SCENARIOS = {
+    # BASELINE config 1 at its real size
+    "c1_full": dict(kind="depth", scene="room", frames=30, width=320, height=240, edge=0.08,
+                    tau=0.03, caps=(200000, 100000), n_hash=1000003, sigma=2.5e-5, cadence=10),
+    # BASELINE config 2 geometry: large room, 640x480 @ 5 mm, bench input format;
+    # the first two frames of the bench's 500-frame sweep
+    "c2_large_frame": dict(kind="depth", scene="large_room", frames=2, width=640, height=480,
+                           edge=0.04, tau=0.015, caps=(160000, 20000), n_hash=4000037,
+                           sigma=2.5e-5, cadence=2, depth_dtype="float32", color_dtype="uint8",
+                           sweep=500),
+    # BASELINE config 3: one full 128-beam scan
+    "c3_scan": dict(kind="lidar", scans=1, beams=128, columns=2048, edge=1.6, tau=0.8,
+                    caps=(160000, 40000), n_hash=4000037, sigma=1e-2, cadence=1),
+}
+
+
+def run_full_scenario(backend, name, mesh=False):
+    """Run one FULL_SCENARIOS entry on a backend; returns the golden record
+    (stats, merges, levels, digests; mesh digests for depth when asked)."""
+    spec = dict(FULL_SCENARIOS[name])
+    kind = spec.pop("kind")
+    if kind == "depth":
+        spec["depth_dtype"] = np.dtype(spec.get("depth_dtype", "float64")).type
+        spec["color_dtype"] = np.dtype(spec.get("color_dtype", "float64")).type
+        b, stats, merges, seq = run_depth_scenario(backend, **spec)
+        inp = array_digest(*[np.asarray(f.depth) for f in seq],
+                           *[np.asarray(f.color) for f in seq if f.color is not None])
+    else:
+        b, stats, merges, seq = run_lidar_scenario(backend, **spec)
+        inp = array_digest(*[np.asarray(f.points) for f in seq])
+    st = b.state()
+    out = {"stats": stats, "merges": merges, "levels": level_summary(st),
+           "keys_digest": keys_digest(st), "state_digest": state_digest(st),
+           "input_digest": inp}
+    if mesh and kind == "depth" and name == "c1_full":
+        v, n, c, t = b.mesh()
+        out["mesh"] = {"nv": int(len(v)), "nt": int(len(t)), "digest": mesh_digest(v, t),
+                       "full_digest": array_digest(v, n, c, t)}
+    if hasattr(b, "close"):
+        b.close()
+    return out
