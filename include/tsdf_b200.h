@@ -95,6 +95,24 @@ int tsdf_table_set_shard(tsdf_table *t, int32_t rank, int32_t world);
  * Lets a dataset's 16-bit PNG depth cross PCIe at 2 B/px. */
 int tsdf_table_set_depth_scale(tsdf_table *t, double depth_scale);
 
+/* LiDAR hot-block update order (integrate_pointcloud, integrate.py:175-252).
+ * TSDF_LIDAR_ORDERED (default): every voxel applies its observations in ray
+ * order, the reference's _apply_batch arrival order (integrate.py:92-119):
+ * bit-identical state.  TSDF_LIDAR_CHUNKED: blocks crossed by more than 256
+ * near rays fold each voxel's observations in groups of 512 rays into partial
+ * Welford states, merged with the voxel's prior state in ray order by Chan's
+ * pairwise formula -- the same mean / sum of squared deviations up to
+ * rounding (the north star's 1e-4 relative TSDF / variance tolerance), exact
+ * weights and block keys, and levels audited by tsdf_table_merge_audit.
+ * Only without a weight cap; capped calls always run ordered. */
+#define TSDF_LIDAR_ORDERED 0
+#define TSDF_LIDAR_CHUNKED 1
+int tsdf_table_set_lidar_mode(tsdf_table *t, int32_t mode);
+/* Merge passes so far: level decisions whose block mean variance lay within
+ * 1e-6 relative of sigma (adapt.py:41-72) -- the only decisions rounding
+ * differences of the chunked mode could flip.  0 = levels provably exact. */
+int tsdf_table_merge_audit(tsdf_table *t, int64_t *near_threshold);
+
 /* integrate_depth(table, DepthFrame, tau, weight_cap) -- integrate.py:255-342.
  * depth: H*W z-depth in metres (0 / NaN invalid); rgb: H*W*3 or NULL.
  * K = (fx, fy, cx, cy); R row-major 3x3 and t (3) are world-from-sensor

@@ -86,6 +86,8 @@ def lib():
     L.tsdf_table_reset.argtypes = [_ptr]
     L.tsdf_table_set_shard.argtypes = [_ptr, i32, i32]
     L.tsdf_table_set_depth_scale.argtypes = [_ptr, C.c_double]
+    L.tsdf_table_set_lidar_mode.argtypes = [_ptr, i32]
+    L.tsdf_table_merge_audit.argtypes = [_ptr, C.POINTER(C.c_int64)]
     L.tsdf_integrate_depth.argtypes = [_ptr, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p, _f64p,
                                        _f64p, dbl, dbl, C.POINTER(IntegrationStatsC)]
     L.tsdf_integrate_depth_batch.argtypes = [_ptr, i32, _ptr, i32, _ptr, i32, i32, i32, i32,

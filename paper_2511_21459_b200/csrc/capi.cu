@@ -84,6 +84,22 @@ int tsdf_table_set_depth_scale(tsdf_table* t, double depth_scale) {
   return TSDF_OK;
 }
 
+int tsdf_table_set_lidar_mode(tsdf_table* t, int32_t mode) {
+  NEED(t);
+  if (mode != TSDF_LIDAR_ORDERED && mode != TSDF_LIDAR_CHUNKED) {
+    set_error("lidar mode must be TSDF_LIDAR_ORDERED (0) or TSDF_LIDAR_CHUNKED (1)");
+    return TSDF_EVALUE;
+  }
+  T_(t)->lidar_mode = mode;
+  return TSDF_OK;
+}
+
+int tsdf_table_merge_audit(tsdf_table* t, int64_t* near_threshold) {
+  NEED(t);
+  *near_threshold = (int64_t)T_(t)->merge_audit;
+  return TSDF_OK;
+}
+
 int tsdf_integrate_depth(tsdf_table* t, const void* depth, int32_t depth_dtype, const void* rgb,
                          int32_t rgb_dtype, int32_t height, int32_t width, int32_t mem,
                          const double* K, const double* R, const double* trans, double tau,

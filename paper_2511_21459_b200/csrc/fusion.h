@@ -46,6 +46,12 @@ struct Table {
   // synchronises; maintain_table() rebuilds the index once it passes slots/4
   unsigned long long* htomb = nullptr;
   uint64_t rehashes = 0;
+  size_t l2_window = 0;
+  // LiDAR hot-segment mode: 0 = ordered (bit-exact ray order), 1 = chunked
+  // (partial Welford states merged by Chan's formula; tsdf_table_set_lidar_mode)
+  int lidar_mode = 0;
+  // merge-pass audit: level decisions within 1e-6 relative of sigma so far
+  uint64_t merge_audit = 0;  // bytes of keys[] under the persisting L2 window (0: none)
   uint32_t call_id = 0;
   double depth_scale = 1.0;  // raw u16 depth units per metre (tsdf_table_set_depth_scale)
   Buf mesh_out;                   // the last extract_mesh_begin result (device)

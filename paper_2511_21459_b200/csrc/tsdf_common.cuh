@@ -126,6 +126,7 @@ struct MergeDev {
   unsigned long long n_dirty;  // dirty-list length at the pass (snapshot)
   uint32_t skip;
   uint32_t pad;  // k_merge_apply: 1 = a merged weight was rounded to binary32
+  unsigned long long audit;  // level decisions within 1e-6 relative of sigma
 };
 
 __host__ __device__ inline uint64_t pack_key(int64_t x, int64_t y, int64_t z) {

@@ -177,6 +177,25 @@ class HashTable:
             N.check(N.lib().tsdf_table_set_depth_scale(self._h, depth_scale), "set_depth_scale")
             self._depth_scale = depth_scale
 
+    def set_lidar_mode(self, mode: str) -> None:
+        """LiDAR hot-block update order: "ordered" (default; bit-identical to
+        the reference's ray-order Welford chain) or "chunked" (observations
+        folded in 512-ray groups and merged by Chan's formula -- TSDF /
+        variance within rounding, exact weights, keys and audited levels;
+        include/tsdf_b200.h)."""
+        modes = {"ordered": 0, "chunked": 1}
+        if mode not in modes:
+            raise ValueError(f"lidar mode must be one of {sorted(modes)}")
+        N.check(N.lib().tsdf_table_set_lidar_mode(self._h, modes[mode]), "set_lidar_mode")
+        self._lidar_mode = mode
+
+    def merge_audit(self) -> int:
+        """Level decisions so far within 1e-6 relative of sigma (0: every
+        level is robust to the chunked mode's rounding)."""
+        out = C.c_int64(0)
+        N.check(N.lib().tsdf_table_merge_audit(self._h, C.byref(out)), "merge_audit")
+        return int(out.value)
+
     def reset(self) -> None:
         N.check(N.lib().tsdf_table_reset(self._h), "reset")
 

@@ -585,3 +585,40 @@ def test_lidar_weight_cap_hot_segments_vs_oracle(weight_cap, color):
     assert_states_match(g.state(), o.state())
     w = g.state()[0][2]
     assert w.max() == weight_cap
+
+
+def test_lidar_chunked_mode_within_tolerance_vs_oracle():
+    """TSDF_LIDAR_CHUNKED (hot blocks folded in 512-ray groups, merged by
+    Chan's formula) against the ORDERED oracle over 4 full config-3 scans with
+    colour and two merge passes: counters, block keys, levels and weights
+    exact; TSDF / variance within the north star's 1e-4 relative; colour
+    within 1e-4; the level audit empty (integrate.py:92-119, adapt.py:41-72)."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    scans = synth.lidar_frames(4, 128, 2048)
+    rng = np.random.default_rng(11)
+    for s in scans:
+        s.colors = rng.integers(0, 256, (len(s.points), 3)).astype(np.uint8)
+    caps, nh = (500000, 60000), 4000037
+    g = PU.GpuBackend(nh, 1.6, caps)
+    g.t.set_lidar_mode("chunked")
+    o = PU.OracleBackend(nh, 1.6, caps)
+    for i, s in enumerate(scans):
+        assert g.points(s, 0.8) == o.points(s, 0.8)
+        if i % 2 == 1:
+            assert g.merge(1e-2) == o.merge(1e-2)
+    a, b = g.state(), o.state()
+    assert set(a) == set(b)
+    diff = 0
+    for level in a:
+        ca, ta, wa, sa, cola = a[level]
+        cb, tb, wb, sb, colb = b[level]
+        assert np.array_equal(ca, cb), f"level {level}: block keys differ"
+        assert np.array_equal(wa, wb), f"level {level}: weights differ"
+        assert np.all(np.abs(ta - tb) <= TOL_REL * np.abs(tb) + 1e-7 * 0.8)
+        assert np.all(np.abs(sa - sb) <= TOL_REL * np.abs(sb) + 1e-10 * 0.64 * wb)
+        assert np.all(np.abs(cola - colb) <= 1e-4)
+        diff += int(np.count_nonzero(ta != tb))
+    assert diff > 0, "chunked mode did not engage (no hot block differs from the ordered chain)"
+    assert g.t.merge_audit() == 0
+    g.close()
