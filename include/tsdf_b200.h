@@ -294,6 +294,28 @@ int tsdf_dda_blocks(const double *origins, const double *endpoints, int64_t n,
  * level-0 blocks apply_merges would re-home; *coords malloc'd. */
 int tsdf_merge_candidates(tsdf_table *t, double sigma_threshold, double min_eligible_fraction,
                           double min_mean_weight, int64_t **coords, int64_t *n_out);
+/* Sharded extraction with a halo (sharding.extract_mesh_halo; the multi-GPU
+ * split of extract_mesh, meshing.py:412-487).
+ * _block_summary: every live block of this table -- packed key (21 bits per
+ * axis), level, observed flag and observed tsdf range (meshing.py:428-438),
+ * the inputs of the 27-neighbourhood kept test (:440-456).
+ * _emit_keys: Marching Cubes output before the vertex dedup (positions in
+ * half-voxel lattice units, unnormalised normals, colours, triangles), in
+ * the reference's emission order, for a caller-given kept list: packed keys
+ * in canonical order, level_counts[l] at level l, each level's list
+ * starting on a 256-block chunk boundary of the map's kept list; every kept
+ * block and its 26 live neighbours must be in the table.  Free with
+ * tsdf_mesh_free.
+ * _finish: the exact dedup, winding fix and epsilon collapse over
+ * concatenated _emit_keys outputs (triangle indices offset) -- the mesh
+ * tsdf_extract_mesh returns for the whole map (eps < 0: the default). */
+int tsdf_mesh_block_summary(tsdf_table *t, uint64_t *keys, int32_t *levels, uint8_t *observed,
+                            double *tsdf_lo, double *tsdf_hi, int64_t cap, int64_t *n_out);
+int tsdf_mesh_emit_keys(tsdf_table *t, const uint64_t *keys, const int64_t *level_counts, double iso,
+                        tsdf_mesh *raw);
+int tsdf_mesh_finish(const double *vertices, const double *normals, const double *colors, int64_t nv,
+                     const int64_t *triangles, int64_t nt, double block_edge, double epsilon,
+                     tsdf_mesh *out);
 /* collapse_vertices (meshing.py:502-552) on the device */
 int tsdf_collapse_vertices(const double *vertices, const double *normals, const double *colors,
                            int64_t nv, const int64_t *triangles, int64_t nt, double epsilon,

@@ -142,6 +142,9 @@ def lib():
     L.tsdf_merge_candidates.argtypes = [_ptr, dbl, dbl, dbl, C.POINTER(C.POINTER(i64)),
                                         C.POINTER(i64)]
     L.tsdf_collapse_vertices.argtypes = [_ptr, _ptr, _ptr, i64, _ptr, i64, dbl, C.POINTER(MeshC)]
+    L.tsdf_mesh_block_summary.argtypes = [_ptr, _ptr, _ptr, _ptr, _ptr, _ptr, i64, C.POINTER(i64)]
+    L.tsdf_mesh_emit_keys.argtypes = [_ptr, _ptr, _ptr, dbl, C.POINTER(MeshC)]
+    L.tsdf_mesh_finish.argtypes = [_ptr, _ptr, _ptr, i64, _ptr, i64, dbl, dbl, C.POINTER(MeshC)]
     L.tsdf_free.argtypes = [_ptr]
     L.tsdf_profile_enable.argtypes = [_ptr, i32]
     L.tsdf_work_totals.argtypes = [_ptr, _i64p, i32]

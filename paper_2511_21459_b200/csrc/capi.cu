@@ -271,6 +271,41 @@ void tsdf_mesh_free(tsdf_mesh* m) {
   memset(m, 0, sizeof(*m));
 }
 
+static void to_c_mesh(const MeshOut& m, tsdf_mesh* out) {
+  out->vertices = m.v;
+  out->normals = m.n;
+  out->colors = m.c;
+  out->num_vertices = m.nv;
+  out->triangles = m.tri;
+  out->num_triangles = m.nt;
+}
+
+int tsdf_mesh_block_summary(tsdf_table* t, uint64_t* keys, int32_t* levels, uint8_t* observed,
+                            double* tsdf_lo, double* tsdf_hi, int64_t cap, int64_t* n_out) {
+  NEED(t);
+  return mesh_block_summary(T_(t), keys, levels, observed, tsdf_lo, tsdf_hi, cap, n_out);
+}
+
+int tsdf_mesh_emit_keys(tsdf_table* t, const uint64_t* keys, const int64_t* level_counts, double iso,
+                        tsdf_mesh* raw) {
+  NEED(t);
+  memset(raw, 0, sizeof(*raw));
+  MeshOut m{};
+  int s = mesh_emit_keys(T_(t), keys, level_counts, iso, &m);
+  to_c_mesh(m, raw);
+  return s;
+}
+
+int tsdf_mesh_finish(const double* v, const double* n, const double* c, int64_t nv, const int64_t* tri,
+                     int64_t nt, double block_edge, double eps, tsdf_mesh* out) {
+  memset(out, 0, sizeof(*out));
+  if (eps < 0) eps = 0.25 * (block_edge / kFineSide);
+  MeshOut m{};
+  int s = mesh_finish(v, n, c, nv, tri, nt, block_edge, eps, &m);
+  to_c_mesh(m, out);
+  return s;
+}
+
 int tsdf_find_batch(tsdf_table* t, const int64_t* coords, int64_t n, int64_t* handles,
                     int32_t* levels, uint8_t* found) {
   NEED(t);

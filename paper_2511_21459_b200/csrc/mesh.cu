@@ -863,18 +863,13 @@ static int collapse_device(Scratch& S, const double* v, const double* nrm, const
   return kOk;
 }
 
-static int extract_mesh_dev(Table* T, double iso, double eps, DevMesh* out) {
-  *out = DevMesh{};
-  if (eps < 0) {
-    set_error("epsilon must be non-negative");
-    return kValueError;
-  }
-  if (int s = load_tables()) return s;
+// M1-M3: the kept blocks of the table in canonical order (packed keys ascend
+// within a level, levels concatenated); loff[l] .. loff[l+1] is level l
+static int kept_blocks(Table* T, Scratch& S, double iso, uint64_t** skeys_out, uint32_t** sslots_out,
+                       int64_t* loff) {
   cudaStream_t st = T->stream;
-  MCK(cudaStreamSynchronize(st));
   const DevTable& d = T->d;
   uint64_t slots = T->slots;
-  Scratch S(st);
   uint8_t* obs = S.bufs.get<uint8_t>(slots);
   double* rlo = S.bufs.get<double>(slots);
   double* rhi = S.bufs.get<double>(slots);
@@ -906,36 +901,60 @@ static int extract_mesh_dev(Table* T, double iso, double eps, DevMesh* out) {
   unsigned long long hcnt[kMaxLevels];
   MCK(cudaMemcpyAsync(hcnt, kcnt, sizeof(hcnt), cudaMemcpyDeviceToHost, st));
   MCK(cudaStreamSynchronize(st));
-  // canonical order per level, concatenated; chunks of 256 within a level
   uint64_t nb = 0;
   for (int l = 0; l < d.n_levels; l++) nb += hcnt[l];
+  *skeys_out = nullptr;
+  *sslots_out = nullptr;
+  loff[0] = 0;
+  for (int l = 0; l < d.n_levels; l++) loff[l + 1] = loff[l] + (int64_t)hcnt[l];
   if (nb == 0) return kOk;
   uint64_t* skeys = S.bufs.get<uint64_t>(nb);
   uint32_t* sslots = S.bufs.get<uint32_t>(nb);
+  if (!skeys || !sslots) return kCapacityError;
+  for (int l = 0; l < d.n_levels; l++) {
+    const uint64_t n = hcnt[l];
+    if (!n) continue;
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, kkeys + l * cap, skeys + loff[l], kslots + l * cap,
+                                    sslots + loff[l], (int64_t)n, 0, 63, st);
+    if (int s = S.need(b)) return s;
+    MCK(cub::DeviceRadixSort::SortPairs(S.tmp, b, kkeys + l * cap, skeys + loff[l], kslots + l * cap,
+                                        sslots + loff[l], (int64_t)n, 0, 63, st));
+  }
+  *skeys_out = skeys;
+  *sslots_out = sslots;
+  return kOk;
+}
+
+// raw Marching Cubes output in the reference's emission order: lattice-unit
+// positions, unnormalised normals, colours and triangles before the vertex
+// dedup (device arrays in the scratch)
+struct RawDev {
+  double *v = nullptr, *n = nullptr, *c = nullptr;
+  int64_t* tri = nullptr;
+  int64_t nv = 0, nt = 0;
+};
+
+// M4-M6 over kept blocks given as slots in canonical order with level
+// offsets loff[0..n_levels]; chunks of 256 restart at every level
+static int emit_raw(Table* T, Scratch& S, const uint32_t* sslots, const int64_t* loff, double iso,
+                    RawDev* raw) {
+  *raw = RawDev{};
+  cudaStream_t st = T->stream;
+  const DevTable& d = T->d;
+  const uint64_t nb = (uint64_t)loff[d.n_levels];
+  if (nb == 0) return kOk;
   int32_t* blevel = S.bufs.get<int32_t>(nb);
-  if (!skeys || !sslots || !blevel) return kCapacityError;
+  if (!blevel) return kCapacityError;
   ChunkMeta CM{};
   CM.n_levels = d.n_levels;
   uint64_t nchunks = 0;
-  {
-    uint64_t off = 0;
-    for (int l = 0; l < d.n_levels; l++) {
-      const uint64_t n = hcnt[l];
-      CM.loff[l] = (int64_t)off;
-      CM.cbase[l] = (int64_t)nchunks;
-      if (n) {
-        size_t b = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, b, kkeys + l * cap, skeys + off, kslots + l * cap,
-                                        sslots + off, (int64_t)n, 0, 63, st);
-        if (int s = S.need(b)) return s;
-        MCK(cub::DeviceRadixSort::SortPairs(S.tmp, b, kkeys + l * cap, skeys + off, kslots + l * cap,
-                                            sslots + off, (int64_t)n, 0, 63, st));
-      }
-      off += n;
-      nchunks += (n + 255) / 256;
-    }
-    CM.loff[d.n_levels] = (int64_t)off;
+  for (int l = 0; l < d.n_levels; l++) {
+    CM.loff[l] = loff[l];
+    CM.cbase[l] = (int64_t)nchunks;
+    nchunks += (uint64_t)(loff[l + 1] - loff[l] + 255) / 256;
   }
+  CM.loff[d.n_levels] = loff[d.n_levels];
   int64_t* chunk_of = S.bufs.get<int64_t>(nb);
   int64_t* chunk_start = S.bufs.get<int64_t>(nchunks);
   int32_t* chunk_size = S.bufs.get<int32_t>(nchunks);
@@ -1012,27 +1031,204 @@ static int extract_mesh_dev(Table* T, double iso, double eps, DevMesh* out) {
   }
   T->launches++;
   MCK(cudaGetLastError());
-  // exact dedup of bit-identical boundary vertices
-  uint64_t nv = (uint64_t)vtot, nt = (uint64_t)ttot;
+  *raw = RawDev{vpos, vnrm, vcol, tri, vtot, ttot};
+  return kOk;
+}
+
+// M7: exact dedup of bit-identical vertices (normals summed in emission
+// order), winding fix, epsilon collapse and compaction
+static int finish_raw(Scratch& S, const RawDev& r, double edge, double eps, cudaStream_t st,
+                      DevMesh* out, Buf* keep) {
+  *out = DevMesh{};
+  if (r.nt == 0) return kOk;
+  const uint64_t nv = (uint64_t)r.nv, nt = (uint64_t)r.nt;
   uint64_t* idx = S.bufs.get<uint64_t>(nv);
   int64_t* inv = S.bufs.get<int64_t>(nv);
   int64_t* gst = S.bufs.get<int64_t>(nv);
   if (!idx || !inv || !gst) return kCapacityError;
   int64_t ng = 0;
-  if (int s = unique_rows<double, true>(S, vpos, nv, idx, inv, gst, &ng, st)) return s;
+  if (int s = unique_rows<double, true>(S, r.v, nv, idx, inv, gst, &ng, st)) return s;
   double* mv = S.bufs.get<double>(3 * ng);
   double* mn = S.bufs.get<double>(3 * ng);
   double* mc = S.bufs.get<double>(3 * ng);
   int64_t* mt = S.bufs.get<int64_t>(3 * nt);
   if (!mv || !mn || !mc || !mt) return kCapacityError;
-  double scale = d.edge / 16.0;
-  k_dedup_out<<<gridn(ng), 256, 0, st>>>(vpos, vnrm, vcol, idx, gst, ng, nv, scale, mv, mn, mc);
-  k_orient<<<gridn(nt), 256, 0, st>>>(tri, inv, nt, mv, mn, mt);
-  T->launches += 12;
+  k_dedup_out<<<gridn(ng), 256, 0, st>>>(r.v, r.n, r.c, idx, gst, ng, nv, edge / 16.0, mv, mn, mc);
+  k_orient<<<gridn(nt), 256, 0, st>>>(r.tri, inv, nt, mv, mn, mt);
   MCK(cudaGetLastError());
-  int s = collapse_device(S, mv, mn, mc, (uint64_t)ng, mt, nt, eps, st, out, &T->mesh_out);
+  return collapse_device(S, mv, mn, mc, (uint64_t)ng, mt, nt, eps, st, out, keep);
+}
+
+static int extract_mesh_dev(Table* T, double iso, double eps, DevMesh* out) {
+  *out = DevMesh{};
+  if (eps < 0) {
+    set_error("epsilon must be non-negative");
+    return kValueError;
+  }
+  if (int s = load_tables()) return s;
+  cudaStream_t st = T->stream;
+  MCK(cudaStreamSynchronize(st));
+  Scratch S(st);
+  uint64_t* skeys;
+  uint32_t* sslots;
+  int64_t loff[kMaxLevels + 1];
+  if (int s = kept_blocks(T, S, iso, &skeys, &sslots, loff)) return s;
+  RawDev raw;
+  if (int s = emit_raw(T, S, sslots, loff, iso, &raw)) return s;
+  T->launches += 12;
+  int s = finish_raw(S, raw, T->d.edge, eps, st, out, &T->mesh_out);
   prof_collect(T);
   return s;
+}
+
+// ---- sharded extraction with a halo (sharding.extract_mesh_halo) -----------
+
+// the per-block summary the kept-set decision needs (meshing.py:428-456):
+// packed key, level, "observed" flag and observed tsdf range of every live
+// block of this table
+__global__ void k_block_summary(DevTable t, const uint8_t* obs, const double* rlo, const double* rhi,
+                                uint64_t* keys, int32_t* levels, uint8_t* o, double* lo, double* hi,
+                                unsigned long long* n) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s <= t.mask;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = t.keys[s];
+    const uint32_t v = t.vals[s];
+    if (!key_live(k) || v == kPending) continue;
+    const unsigned long long i = atomicAdd(n, 1ull);
+    keys[i] = k;
+    levels[i] = val_level(v);
+    o[i] = obs[s];
+    lo[i] = rlo[s];
+    hi[i] = rhi[s];
+  }
+}
+
+int mesh_block_summary(Table* T, uint64_t* keys, int32_t* levels, uint8_t* obs_out, double* lo,
+                       double* hi, int64_t cap, int64_t* n_out) {
+  *n_out = 0;
+  cudaStream_t st = T->stream;
+  MCK(cudaStreamSynchronize(st));
+  Scratch S(st);
+  const uint64_t slots = T->slots;
+  uint8_t* obs = S.bufs.get<uint8_t>(slots);
+  double* rlo = S.bufs.get<double>(slots);
+  double* rhi = S.bufs.get<double>(slots);
+  int64_t total = 0;
+  for (int l = 0; l < T->d.n_levels; l++) {
+    int64_t nl = 0;
+    if (int s = live_count(T, l, &nl)) return s;
+    total += nl;
+  }
+  if (total > cap) {
+    set_error("mesh_block_summary: output arrays too small");
+    return kValueError;
+  }
+  const uint64_t m = (uint64_t)std::max<int64_t>(total, 1);
+  uint64_t* dk = S.bufs.get<uint64_t>(m);
+  int32_t* dl = S.bufs.get<int32_t>(m);
+  uint8_t* dob = S.bufs.get<uint8_t>(m);
+  double* dlo = S.bufs.get<double>(m);
+  double* dhi = S.bufs.get<double>(m);
+  unsigned long long* dn = S.bufs.get<unsigned long long>(1);
+  if (!obs || !rlo || !rhi || !dk || !dl || !dob || !dlo || !dhi || !dn) return kCapacityError;
+  MCK(cudaMemsetAsync(dn, 0, 8, st));
+  k_block_range<<<148 * 16, 256, 0, st>>>(T->d, obs, rlo, rhi);
+  k_block_summary<<<gridn(slots), 256, 0, st>>>(T->d, obs, rlo, rhi, dk, dl, dob, dlo, dhi, dn);
+  T->launches += 2;
+  unsigned long long hn = 0;
+  MCK(cudaMemcpyAsync(&hn, dn, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  if (hn) {
+    MCK(cudaMemcpyAsync(keys, dk, hn * 8, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(levels, dl, hn * 4, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(obs_out, dob, hn, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(lo, dlo, hn * 8, cudaMemcpyDeviceToHost, st));
+    MCK(cudaMemcpyAsync(hi, dhi, hn * 8, cudaMemcpyDeviceToHost, st));
+    MCK(cudaStreamSynchronize(st));
+  }
+  *n_out = (int64_t)hn;
+  return kOk;
+}
+
+__global__ void k_find_slots(DevTable t, const uint64_t* keys, uint64_t n, uint32_t* slots,
+                             unsigned long long* missing) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t s = table_find(t, keys[i]);
+    if (s < 0) atomicAdd(missing, 1ull);
+    slots[i] = s < 0 ? 0u : (uint32_t)s;
+  }
+}
+
+// raw emission (pre-dedup) for a caller-given kept list: `keys` packed, in
+// canonical order per level, level_counts[l] of them at level l; every key
+// and its 26 neighbours present in this table must be the map's own
+int mesh_emit_keys(Table* T, const uint64_t* keys, const int64_t* level_counts, double iso,
+                   MeshOut* out) {
+  memset(out, 0, sizeof(*out));
+  if (int s = load_tables()) return s;
+  cudaStream_t st = T->stream;
+  MCK(cudaStreamSynchronize(st));
+  Scratch S(st);
+  int64_t loff[kMaxLevels + 1];
+  loff[0] = 0;
+  for (int l = 0; l < T->d.n_levels; l++) loff[l + 1] = loff[l] + level_counts[l];
+  const uint64_t nb = (uint64_t)loff[T->d.n_levels];
+  if (nb == 0) return kOk;
+  uint64_t* dk = S.bufs.get<uint64_t>(nb);
+  uint32_t* ds = S.bufs.get<uint32_t>(nb);
+  unsigned long long* miss = S.bufs.get<unsigned long long>(1);
+  if (!dk || !ds || !miss) return kCapacityError;
+  MCK(cudaMemcpyAsync(dk, keys, nb * 8, cudaMemcpyHostToDevice, st));
+  MCK(cudaMemsetAsync(miss, 0, 8, st));
+  k_find_slots<<<gridn(nb), 256, 0, st>>>(T->d, dk, nb, ds, miss);
+  T->launches++;
+  unsigned long long hm = 0;
+  MCK(cudaMemcpyAsync(&hm, miss, 8, cudaMemcpyDeviceToHost, st));
+  MCK(cudaStreamSynchronize(st));
+  if (hm) {
+    set_error("mesh_emit_keys: " + std::to_string(hm) + " kept blocks are not in the table");
+    return kNotFound;
+  }
+  RawDev raw;
+  if (int s = emit_raw(T, S, ds, loff, iso, &raw)) return s;
+  if (raw.nt == 0) return kOk;
+  DevMesh m;
+  m.nv = raw.nv;
+  m.nt = raw.nt;
+  m.base = S.bufs.get<char>(DevMesh::bytes(raw.nv, raw.nt));
+  if (!m.base) return kCapacityError;
+  MCK(cudaMemcpyAsync(m.v(), raw.v, raw.nv * 24, cudaMemcpyDeviceToDevice, st));
+  MCK(cudaMemcpyAsync(m.n(), raw.n, raw.nv * 24, cudaMemcpyDeviceToDevice, st));
+  MCK(cudaMemcpyAsync(m.c(), raw.c, raw.nv * 24, cudaMemcpyDeviceToDevice, st));
+  MCK(cudaMemcpyAsync(m.tri(), raw.tri, raw.nt * 24, cudaMemcpyDeviceToDevice, st));
+  return mesh_to_malloc(m, st, out);
+}
+
+// M7 over raw arrays concatenated from several mesh_emit_keys calls (their
+// triangle indices already offset): the same final mesh as extract_mesh
+int mesh_finish(const double* v, const double* n, const double* c, int64_t nv, const int64_t* tri,
+                int64_t nt, double edge, double eps, MeshOut* out) {
+  memset(out, 0, sizeof(*out));
+  if (eps < 0) {
+    set_error("epsilon must be non-negative");
+    return kValueError;
+  }
+  if (nt == 0 || nv == 0) return kOk;
+  Scratch S;
+  double* dv = S.bufs.get<double>(3 * nv);
+  double* dn = S.bufs.get<double>(3 * nv);
+  double* dc = S.bufs.get<double>(3 * nv);
+  int64_t* dt = S.bufs.get<int64_t>(3 * nt);
+  if (!dv || !dn || !dc || !dt) return kCapacityError;
+  MCK(cudaMemcpy(dv, v, nv * 24, cudaMemcpyHostToDevice));
+  MCK(cudaMemcpy(dn, n, nv * 24, cudaMemcpyHostToDevice));
+  MCK(cudaMemcpy(dc, c, nv * 24, cudaMemcpyHostToDevice));
+  MCK(cudaMemcpy(dt, tri, nt * 24, cudaMemcpyHostToDevice));
+  RawDev raw{dv, dn, dc, dt, nv, nt};
+  DevMesh m;
+  if (int s = finish_raw(S, raw, edge, eps, 0, &m, nullptr)) return s;
+  return mesh_to_malloc(m, 0, out);
 }
 
 int extract_mesh(Table* T, double iso, double eps, MeshOut* out) {

@@ -105,6 +105,54 @@ def collapse_vertices(mesh: Mesh, epsilon: float) -> Mesh:
     return _mesh_from_c(m)
 
 
+# ---- staged extraction (sharding.extract_mesh_halo) -------------------------
+
+def block_summary(table: HashTable) -> dict:
+    """Every live block of the table: packed key (u64, 21 bits per axis),
+    level, observed flag and observed tsdf range -- the inputs of the
+    reference's kept-block test (meshing.py:428-456)."""
+    cap = max(1, table.live_count())
+    out = {"keys": np.empty(cap, np.uint64), "levels": np.empty(cap, np.int32),
+           "obs": np.empty(cap, np.uint8), "lo": np.empty(cap, np.float64),
+           "hi": np.empty(cap, np.float64)}
+    n = C.c_int64()
+    N.check(N.lib().tsdf_mesh_block_summary(table._h, out["keys"].ctypes.data, out["levels"].ctypes.data,
+                                            out["obs"].ctypes.data, out["lo"].ctypes.data,
+                                            out["hi"].ctypes.data, cap, C.byref(n)), "mesh_block_summary")
+    return {k: v[:n.value].copy() for k, v in out.items()}
+
+
+def emit_raw(table: HashTable, keys, level_counts, iso: float = 0.0) -> Mesh:
+    """Marching Cubes output before the vertex dedup (lattice-unit positions,
+    unnormalised normals, triangles into the raw vertex list) for a kept list
+    in canonical order (include/tsdf_b200.h tsdf_mesh_emit_keys)."""
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    lc = np.zeros(4, dtype=np.int64)
+    lc[:len(level_counts)] = level_counts
+    m = N.MeshC()
+    N.check(N.lib().tsdf_mesh_emit_keys(table._h, k.ctypes.data, lc.ctypes.data, float(iso), C.byref(m)),
+            "mesh_emit_keys")
+    return _mesh_from_c(m)
+
+
+def finish_raw(raws, block_edge: float, collapse_epsilon=None) -> Mesh:
+    """Concatenate raw emissions (in emission order) and run the exact vertex
+    dedup, winding fix and epsilon collapse: the extract_mesh result."""
+    raws = [r for r in raws if r.num_triangles]
+    if not raws:
+        return Mesh.empty()
+    offs = np.cumsum([0] + [r.num_vertices for r in raws[:-1]])
+    v = np.ascontiguousarray(np.concatenate([r.vertices for r in raws]))
+    n = np.ascontiguousarray(np.concatenate([r.normals for r in raws]))
+    c = np.ascontiguousarray(np.concatenate([r.colors for r in raws]))
+    t = np.ascontiguousarray(np.concatenate([r.triangles + o for r, o in zip(raws, offs)]), dtype=np.int64)
+    eps = -1.0 if collapse_epsilon is None else float(collapse_epsilon)
+    m = N.MeshC()
+    N.check(N.lib().tsdf_mesh_finish(v.ctypes.data, n.ctypes.data, c.ctypes.data, len(v), t.ctypes.data,
+                                     len(t), float(block_edge), eps, C.byref(m)), "mesh_finish")
+    return _mesh_from_c(m)
+
+
 def effective_cell_extent(level: int, finer_faces, block_edge: float):
     """Per-axis corner planes (metres, block-local) after transition
     truncation (meshing.py:69-88)."""

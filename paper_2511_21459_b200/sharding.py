@@ -319,3 +319,235 @@ def extract_mesh_sharded(table, dist, torch, group=None, device=None, iso: float
     if blobs is None:
         return None
     return extract_mesh(table_from_records(blobs, table), iso=iso, collapse_epsilon=collapse_epsilon)
+
+
+# ---------------------------------------------------------------------------
+# Sharded extraction with a one-block halo (meshing.py:412-487)
+# ---------------------------------------------------------------------------
+# Hash ownership scatters a block's 26 neighbours over every rank, so meshing
+# re-partitions the map spatially instead:
+#   1. every rank summarises its live blocks (key, level, observed flag and
+#      tsdf range: the inputs of the 27-neighbourhood kept test,
+#      meshing.py:428-456) and the summaries are all-gathered (~25 B/block);
+#   2. every rank computes the same plan: the global kept list in canonical
+#      order (packed keys ascending per level), cut into the reference's
+#      256-block chunks (meshing.py:457-459), and a contiguous run of chunks
+#      per rank -- an x-major slab of the map -- plus the live 26-neighbours
+#      of that run (the halo);
+#   3. one all-to-all moves each owner's blocks of every rank's run + halo to
+#      that rank as reference block records;
+#   4. each rank rebuilds its slab + halo in a scratch table and runs the
+#      Marching Cubes passes for its chunks only (raw, pre-dedup output in
+#      the reference's emission order);
+#   5. the raw outputs are gathered in rank (= emission) order and one rank
+#      runs the exact vertex dedup, winding fix and epsilon collapse.
+# Chunk runs start on chunk boundaries and every kept block sees the same 26
+# neighbours as in the full map, so the concatenated raw output equals the
+# single-GPU one and the mesh is bit-identical.
+
+_NBR = np.array([(i // 9 - 1, (i // 3) % 3 - 1, i % 3 - 1) for i in range(27)], dtype=np.int64)
+
+
+def unpack_keys(keys) -> np.ndarray:
+    k = np.asarray(keys, dtype=np.uint64)
+    m = np.uint64((1 << 21) - 1)
+    return np.stack([(k >> np.uint64(42)) & m, (k >> np.uint64(21)) & m, k & m], axis=1).astype(np.int64) - _BIAS
+
+
+def _lookup(sorted_keys, coords):
+    """Index into sorted_keys of each coordinate row, -1 where absent."""
+    c = np.asarray(coords, dtype=np.int64)
+    if len(sorted_keys) == 0:
+        return np.full(len(c), -1, dtype=np.int64)
+    ok = np.all((c >= -_BIAS) & (c < _BIAS), axis=1)
+    k = pack_keys(np.where(ok[:, None], c, 0))
+    i = np.minimum(np.searchsorted(sorted_keys, k), len(sorted_keys) - 1)
+    return np.where(ok & (sorted_keys[i] == k), i, -1)
+
+
+def mesh_plan(summaries, world: int, iso: float = 0.0, n_levels: int = 2) -> dict:
+    """The extraction plan every rank derives from the all-gathered block
+    summaries: canonical kept list per level, each rank's run of whole
+    256-block chunks ('emit': keys + per-level counts) and the blocks each
+    rank needs (its run + live 26-neighbours, 'need': sorted packed keys)."""
+    keys = np.concatenate([s["keys"] for s in summaries]).astype(np.uint64)
+    levels = np.concatenate([s["levels"] for s in summaries]).astype(np.int32)
+    obs = np.concatenate([s["obs"] for s in summaries]).astype(bool)
+    lo = np.concatenate([s["lo"] for s in summaries])
+    hi = np.concatenate([s["hi"] for s in summaries])
+    order = np.argsort(keys, kind="stable")
+    keys, levels, obs, lo, hi = keys[order], levels[order], obs[order], lo[order], hi[order]
+    coords = unpack_keys(keys)
+    # 27-neighbourhood straddle test (meshing.py:440-456; k_keep)
+    nlo = np.full(len(keys), np.inf)
+    nhi = np.full(len(keys), -np.inf)
+    for d in _NBR:
+        j = _lookup(keys, coords + d)
+        use = (j >= 0) & obs[np.maximum(j, 0)]
+        nlo = np.where(use, np.minimum(nlo, lo[np.maximum(j, 0)]), nlo)
+        nhi = np.where(use, np.maximum(nhi, hi[np.maximum(j, 0)]), nhi)
+    kept = obs & (nlo <= iso) & (iso <= nhi)
+    per_level = [keys[kept & (levels == l)] for l in range(n_levels)]  # ascending = canonical
+    # chunks of 256 per level, levels concatenated; contiguous runs per rank
+    chunks = []  # (level, start, stop)
+    for l, kl in enumerate(per_level):
+        chunks += [(l, s, min(s + 256, len(kl))) for s in range(0, len(kl), 256)]
+    total = sum(len(k) for k in per_level)
+    bounds, acc, r = [0], 0, 1
+    for ci, (l, a, b) in enumerate(chunks):
+        acc += b - a
+        if r < world and acc >= total * r / world:
+            bounds.append(ci + 1)
+            r += 1
+    bounds += [len(chunks)] * (world + 1 - len(bounds))
+    emit, need = [], []
+    for rk in range(world):
+        parts = [[] for _ in range(n_levels)]
+        for l, a, b in chunks[bounds[rk]:bounds[rk + 1]]:
+            parts[l].append(per_level[l][a:b])
+        ek = [np.concatenate(p) if p else np.zeros(0, np.uint64) for p in parts]
+        emit.append({"keys": np.concatenate(ek) if ek else np.zeros(0, np.uint64),
+                     "level_counts": [len(x) for x in ek]})
+        allk = emit[-1]["keys"]
+        if len(allk):
+            c = unpack_keys(allk)
+            j = np.concatenate([_lookup(keys, c + d) for d in _NBR])
+            need.append(np.unique(keys[j[j >= 0]]))
+        else:
+            need.append(np.zeros(0, np.uint64))
+    return {"emit": emit, "need": need, "kept": int(total), "chunks": len(chunks), "bounds": bounds}
+
+
+def _records_for(table, keys) -> bytes:
+    """shard_records restricted to the given packed keys."""
+    from .formats import pack_records
+    counts, out = [], []
+    want = np.asarray(keys, dtype=np.uint64)
+    for level in range(table.num_levels):
+        coords, _, t, w, s2, col = table.export_level(level)
+        sel = np.isin(pack_keys(coords), want) if len(coords) else np.zeros(0, bool)
+        counts.append(int(sel.sum()))
+        if counts[-1]:
+            out.append(pack_records(level, coords[sel], t[sel], w[sel], s2[sel], col[sel]).tobytes())
+    return np.asarray([table.num_levels] + counts, dtype="<u8").tobytes() + b"".join(out)
+
+
+def _raw_bytes(m) -> bytes:
+    hdr = np.asarray([m.num_vertices, m.num_triangles], dtype="<i8").tobytes()
+    if not m.num_triangles:
+        return np.asarray([0, 0], dtype="<i8").tobytes()
+    return hdr + b"".join(np.ascontiguousarray(a).tobytes()
+                          for a in (m.vertices, m.normals, m.colors, m.triangles))
+
+
+def _raw_from_bytes(b: bytes):
+    from .meshing import Mesh
+    nv, nt = (int(x) for x in np.frombuffer(b, "<i8", 2, 0))
+    if nt == 0:
+        return Mesh.empty()
+    off = 16
+    arrs = []
+    for n, dt in ((nv, np.float64), (nv, np.float64), (nv, np.float64), (nt, np.int64)):
+        arrs.append(np.frombuffer(b, dt, 3 * n, off).reshape(n, 3))
+        off += 24 * n
+    return Mesh(vertices=arrs[0], normals=arrs[1], colors=arrs[2], triangles=arrs[3])
+
+
+def _mesh_slab(table, plan, rank, blobs, iso):
+    """Step 4 on one rank: its slab + halo in a scratch table, raw emission."""
+    from .meshing import emit_raw
+    e = plan["emit"][rank]
+    if not len(e["keys"]):
+        return _raw_bytes(type("M", (), {"num_triangles": 0})())
+    scratch = table_from_records(blobs, table)
+    try:
+        return _raw_bytes(emit_raw(scratch, e["keys"], e["level_counts"], iso))
+    finally:
+        scratch.close()
+
+
+def _all_gather_bytes(blob: bytes, dist, torch, group=None, device=None):
+    world = dist.get_world_size(group)
+    n = torch.tensor([len(blob)], dtype=torch.int64, device=device)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    cap = max(1, max(sizes))
+    buf = torch.zeros(cap, dtype=torch.uint8, device=device)
+    if blob:
+        buf[:len(blob)] = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(device)
+    parts = [torch.empty(cap, dtype=torch.uint8, device=device) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return [bytes(p[:s].cpu().numpy().tobytes()) for p, s in zip(parts, sizes)]
+
+
+def all_to_all_bytes(blobs, dist, torch, group=None, device=None):
+    """blobs[d] goes to rank d; returns what every rank sent here (by source)."""
+    world = dist.get_world_size(group)
+    send = torch.tensor([len(b) for b in blobs], dtype=torch.int64, device=device)
+    recv = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_to_all_single(recv, send, group=group)
+    rs = [int(x) for x in recv.cpu().tolist()]
+    out_t = torch.empty(max(1, sum(rs)), dtype=torch.uint8, device=device)
+    flat = b"".join(blobs)
+    in_t = torch.zeros(max(1, len(flat)), dtype=torch.uint8, device=device)
+    if flat:
+        in_t[:len(flat)] = torch.frombuffer(bytearray(flat), dtype=torch.uint8).to(device)
+    dist.all_to_all_single(out_t[:sum(rs)] if sum(rs) else out_t[:0], in_t[:len(flat)] if flat else in_t[:0],
+                           output_split_sizes=rs, input_split_sizes=[len(b) for b in blobs], group=group)
+    host = out_t[:sum(rs)].cpu().numpy().tobytes()
+    offs = np.cumsum([0] + rs)
+    return [host[offs[i]:offs[i + 1]] for i in range(world)]
+
+
+def _summary_bytes(s) -> bytes:
+    n = len(s["keys"])
+    return (np.asarray([n], "<i8").tobytes() + s["keys"].astype("<u8").tobytes()
+            + s["levels"].astype("<i4").tobytes() + s["obs"].astype("u1").tobytes()
+            + s["lo"].astype("<f8").tobytes() + s["hi"].astype("<f8").tobytes())
+
+
+def _summary_from_bytes(b: bytes) -> dict:
+    n = int(np.frombuffer(b, "<i8", 1, 0)[0])
+    off = 8
+    out = {}
+    for name, dt, sz in (("keys", "<u8", 8), ("levels", "<i4", 4), ("obs", "u1", 1), ("lo", "<f8", 8),
+                         ("hi", "<f8", 8)):
+        out[name] = np.frombuffer(b, dt, n, off)
+        off += sz * n
+    return out
+
+
+def extract_mesh_halo(table, dist, torch, group=None, device=None, iso: float = 0.0,
+                      collapse_epsilon=None, dst: int = 0):
+    """extract_mesh over the union of the shards with spatially partitioned
+    work and a one-block halo (see above): the Mesh on rank `dst`, None
+    elsewhere.  Bit-identical to extract_mesh of the single-GPU map."""
+    from .meshing import block_summary, finish_raw
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    summ = [_summary_from_bytes(b) for b in
+            _all_gather_bytes(_summary_bytes(block_summary(table)), dist, torch, group, device)]
+    plan = mesh_plan(summ, world, iso, table.num_levels)
+    mine = set(summ[rank]["keys"].tolist())
+    sends = [_records_for(table, [k for k in plan["need"][d].tolist() if k in mine]) for d in range(world)]
+    blobs = all_to_all_bytes(sends, dist, torch, group, device)
+    raw = _mesh_slab(table, plan, rank, blobs, iso)
+    raws = _gather_bytes(raw, dst, dist, torch, group, device)
+    if raws is None:
+        return None
+    return finish_raw([_raw_from_bytes(b) for b in raws], table.block_edge, collapse_epsilon)
+
+
+def extract_mesh_halo_local(tables, iso: float = 0.0, collapse_epsilon=None):
+    """The same protocol over shard tables living in one process (every
+    collective replaced by list plumbing): the single-GPU test of
+    extract_mesh_halo, step for step."""
+    from .meshing import block_summary, finish_raw
+    world = len(tables)
+    summ = [block_summary(t) for t in tables]
+    plan = mesh_plan(summ, world, iso, tables[0].num_levels)
+    owned = [set(s["keys"].tolist()) for s in summ]
+    sends = [[_records_for(tables[o], [k for k in plan["need"][d].tolist() if k in owned[o]])
+              for d in range(world)] for o in range(world)]
+    raws = [_mesh_slab(tables[r], plan, r, [sends[o][r] for o in range(world)], iso) for r in range(world)]
+    return finish_raw([_raw_from_bytes(b) for b in raws], tables[0].block_edge, collapse_epsilon), plan

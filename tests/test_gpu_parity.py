@@ -622,3 +622,41 @@ def test_lidar_chunked_mode_within_tolerance_vs_oracle():
     assert diff > 0, "chunked mode did not engage (no hot block differs from the ordered chain)"
     assert g.t.merge_audit() == 0
     g.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_halo_extraction_equals_single_gpu(world):
+    """Sharded extraction with a one-block halo (SURVEY §8f row 3;
+    sharding.extract_mesh_halo): each shard meshes a contiguous run of the
+    kept list's 256-block chunks from its slab + halo, one rank dedups and
+    collapses the concatenated raw output -- the single-GPU mesh bit for bit
+    on a three-level map (with and without vertex collapse)."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    from paper_2511_21459_b200.sharding import extract_mesh_halo_local
+    frames = synth.render_frames("room", 20, 128, 96, depth_dtype=np.float32, color_dtype=np.uint8)
+    caps = (100000, 20000, 5000)
+    full = P.HashTable(1000003, 10, 7, 0.04, caps)
+    shards = []
+    for r in range(world):
+        t = P.HashTable(1000003, 10, 7, 0.04, caps)
+        t.set_shard(r, world)
+        shards.append(t)
+    for i, f in enumerate(frames):
+        for t in [full] + shards:
+            P.integrate_depth(t, f, 0.015)
+        if (i + 1) % 10 == 0:
+            for t in [full] + shards:
+                P.apply_merges(t, 2.5e-5, all_levels=True)
+    assert full.heaps[1].occupied > 0 and full.heaps[2].occupied > 0
+    for eps in (None, 0.0025):
+        a = P.extract_mesh(full, collapse_epsilon=eps)
+        b, plan = extract_mesh_halo_local(shards, collapse_epsilon=eps)
+        assert a.num_triangles > 1000
+        assert sum(1 for e in plan["emit"] if len(e["keys"])) == min(world, plan["chunks"])
+        for x, y in ((a.vertices, b.vertices), (a.normals, b.normals), (a.colors, b.colors),
+                     (a.triangles, b.triangles)):
+            assert np.array_equal(x, y)
+    # each rank moved its slab + halo, not the map
+    need = sum(len(n) for n in plan["need"])
+    assert need < 2.0 * full.live_count()

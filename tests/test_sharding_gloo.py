@@ -222,3 +222,92 @@ def test_three_rank_variable_size_gather():
         assert p.exitcode == 0
     assert res[0] is None and res[2] is None
     assert res[1] == [bytes(range(r * 7 % 256)) * (r + 1) for r in range(3)]
+
+
+def _bytes_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_21459_b200.sharding import _all_gather_bytes, all_to_all_bytes
+    sends = [bytes([rank, d]) * (3 * d + rank + 1) for d in range(world)]
+    got = all_to_all_bytes(sends, dist, torch)
+    allg = _all_gather_bytes(bytes([rank]) * (rank + 2), dist, torch)
+    q.put((rank, got, allg))
+    dist.destroy_process_group()
+
+
+def test_halo_extraction_byte_collectives_gloo():
+    """The two variable-size collectives of extract_mesh_halo (all-to-all of
+    block records, all-gather of block summaries) on world 3 over gloo."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    ps = [ctx.Process(target=_bytes_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, got, allg = q.get(timeout=120)
+        res[r] = (got, allg)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        got, allg = res[r]
+        assert got == [bytes([o, r]) * (3 * r + o + 1) for o in range(world)]
+        assert allg == [bytes([o]) * (o + 2) for o in range(world)]
+
+
+def test_mesh_plan_partitions_the_kept_list():
+    """mesh_plan (pure host logic): the 27-neighbourhood kept test against a
+    direct evaluation, chunk runs that tile the kept list on 256-block
+    boundaries, and halos that hold every live neighbour of a rank's run."""
+    import numpy as np
+    from paper_2511_21459_b200.sharding import mesh_plan, pack_keys, unpack_keys
+    rng = np.random.default_rng(3)
+    coords = np.unique(rng.integers(-12, 12, size=(6000, 3)), axis=0)
+    keys = pack_keys(coords)
+    n = len(keys)
+    summ = {"keys": keys, "levels": rng.integers(0, 2, n).astype(np.int32),
+            "obs": (rng.random(n) < 0.9).astype(np.uint8),
+            "lo": rng.uniform(-0.05, 0.02, n), "hi": rng.uniform(-0.02, 0.05, n)}
+    parts = [{k: v[i::3] for k, v in summ.items()} for i in range(3)]
+    plan = mesh_plan(parts, 4, 0.0, 2)
+    # direct kept test
+    idx = {tuple(c): i for i, c in enumerate(coords.tolist())}
+    kept = set()
+    for i, c in enumerate(coords.tolist()):
+        if not summ["obs"][i]:
+            continue
+        lo, hi = np.inf, -np.inf
+        for d in np.ndindex(3, 3, 3):
+            j = idx.get((c[0] + d[0] - 1, c[1] + d[1] - 1, c[2] + d[2] - 1))
+            if j is not None and summ["obs"][j]:
+                lo, hi = min(lo, summ["lo"][j]), max(hi, summ["hi"][j])
+        if lo <= 0.0 <= hi:
+            kept.add(int(keys[i]))
+    emitted = np.concatenate([e["keys"] for e in plan["emit"]])
+    assert set(emitted.tolist()) == kept and len(emitted) == len(kept) == plan["kept"]
+    level_of = dict(zip(keys.tolist(), summ["levels"].tolist()))
+    for l in range(2):
+        lvl = np.sort(np.array([k for k in kept if level_of[k] == l], dtype=np.uint64))
+        got = np.concatenate([e["keys"][sum(e["level_counts"][:l]):sum(e["level_counts"][:l + 1])]
+                              for e in plan["emit"]])
+        assert np.array_equal(got, lvl)
+        starts = np.cumsum([0] + [e["level_counts"][l] for e in plan["emit"]])[:-1]
+        assert all(s % 256 == 0 or s == len(lvl) for s in starts)
+    live = set(keys.tolist())
+    for e, need in zip(plan["emit"], plan["need"]):
+        nd = set(need.tolist())
+        for c in unpack_keys(e["keys"]):
+            for d in np.ndindex(3, 3, 3):
+                k = int(pack_keys((c + np.array(d) - 1)[None])[0])
+                if k in live:
+                    assert k in nd
