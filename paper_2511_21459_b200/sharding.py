@@ -83,8 +83,8 @@ class ShardedFusion:
         if self.world == 1:
             return self.engine.extract(iso=iso)
         cfg = self.engine.config
-        return extract_mesh_sharded(self.engine.table, self.dist, self.torch, self.group,
-                                    self.device, iso, cfg.collapse_epsilon_factor * cfg.nu_fine, dst)
+        return extract_mesh_halo(self.engine.table, self.dist, self.torch, self.group,
+                                 self.device, iso, cfg.collapse_epsilon_factor * cfg.nu_fine, dst)
 
     def maybe_merge(self):
         n = self.engine.maybe_merge()
@@ -246,12 +246,16 @@ def integrate_depth_raysharded(table, frame, tau, dist, torch, group=None, devic
 #
 # Corner sampling reads the 26 lattice neighbours of a block (meshing.py:
 # 94-158, 306-310), and with hash ownership nearly every neighbour of a block
-# lives on another rank, so a per-rank halo would be most of the map anyway.
-# The shards therefore gather their blocks (bulk level exports, packed in the
-# reference's block-record layout) onto one GPU, which rebuilds the map in a
-# scratch table and extracts it there.  The mesh depends only on map content
-# (never on heap handles), so it is bit-identical to extracting the
-# single-GPU table.  A large-room map is ~5 GB: one NVLink all-gather.
+# lives on another rank.  Two paths:
+#   * extract_mesh_sharded gathers every shard's blocks (bulk level exports,
+#     packed in the reference's block-record layout) onto one GPU, which
+#     rebuilds the map in a scratch table and extracts it there (simple; the
+#     whole map on one device);
+#   * extract_mesh_halo (below; what ShardedFusion.extract uses) re-partitions
+#     the map spatially: each rank meshes a slab from the slab plus a
+#     one-block halo and only the raw output meets on one rank.
+# The mesh depends only on map content (never on heap handles), so both are
+# bit-identical to extracting the single-GPU table.
 
 def shard_records(table) -> bytes:
     """This shard's live blocks: a header of per-level block counts (u64),
@@ -295,6 +299,7 @@ def _gather_bytes(blob: bytes, dst: int, dist, torch, group=None, device=None):
     """Every rank's byte string on rank `dst` (None elsewhere): lengths,
     then one padded all-gather (NCCL has no variable-size gather)."""
     world = dist.get_world_size(group)
+    device = "cpu" if dist.get_backend(group) == "gloo" else device
     n = torch.tensor([len(blob)], dtype=torch.int64, device=device)
     sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
@@ -466,8 +471,15 @@ def _mesh_slab(table, plan, rank, blobs, iso):
         scratch.close()
 
 
+def _comm_device(dist, group, device):
+    """Where byte payloads travel: host tensors on gloo (CPU tests, ranks
+    sharing one GPU), the rank's device on NCCL."""
+    return "cpu" if dist.get_backend(group) == "gloo" else device
+
+
 def _all_gather_bytes(blob: bytes, dist, torch, group=None, device=None):
     world = dist.get_world_size(group)
+    device = _comm_device(dist, group, device)
     n = torch.tensor([len(blob)], dtype=torch.int64, device=device)
     sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
@@ -484,6 +496,7 @@ def _all_gather_bytes(blob: bytes, dist, torch, group=None, device=None):
 def all_to_all_bytes(blobs, dist, torch, group=None, device=None):
     """blobs[d] goes to rank d; returns what every rank sent here (by source)."""
     world = dist.get_world_size(group)
+    device = _comm_device(dist, group, device)
     send = torch.tensor([len(b) for b in blobs], dtype=torch.int64, device=device)
     recv = torch.empty(world, dtype=torch.int64, device=device)
     dist.all_to_all_single(recv, send, group=group)
