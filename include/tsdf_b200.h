@@ -95,6 +95,38 @@ int tsdf_table_set_shard(tsdf_table *t, int32_t rank, int32_t world);
  * Lets a dataset's 16-bit PNG depth cross PCIe at 2 B/px. */
 int tsdf_table_set_depth_scale(tsdf_table *t, double depth_scale);
 
+/* Ray-sharded merge window for block-key-hash shards: B depth
+ * frames and their merge pass in three stream-ordered calls with one
+ * collective between consecutive calls and a single host synchronisation
+ * (in _update).  Inputs as tsdf_integrate_depth_window.
+ *  _frames: the pixel passes of all frames (d_ray and the min/max pyramid in
+ *           full; the FP64 segment-end span that sets dda.py:63's lock-step
+ *           cap only over this rank's tiles); writes the B partial caps to
+ *           `caps` (device u64[B]).  Caller: all-reduce MAX of caps.
+ *  _walk:   with the reduced caps, this rank's tiles of rays of every frame
+ *           walk and write each block key they meet once per frame into the
+ *           device exchange buffer: for owner o, stride = B * (bucket_cap + 1)
+ *           words, [o*stride + i] = count of frame i, [o*stride + B + i*cap
+ *           + j] = key j.  Caller: all-to-all of the buffer (equal splits of
+ *           stride words).
+ *  _update: `received` (same layout, source-major): per frame in order,
+ *           insert the keys this rank owns, commit the new blocks, update the
+ *           voxels; then one merge pass (sigma > 0); per-frame stats[B] of
+ *           this shard.  A bucket count above bucket_cap is a CapacityError. */
+int tsdf_depth_window_frames(tsdf_table *t, int32_t n_frames, const void *const *depth,
+                             int32_t depth_dtype, const void *const *rgb, int32_t rgb_dtype,
+                             int32_t height, int32_t width, int32_t mem, const double *K,
+                             const double *R, const double *trans, double tau, double weight_cap,
+                             int32_t ray_rank, int32_t ray_world, uint64_t *caps);
+int tsdf_depth_window_walk(tsdf_table *t, const uint64_t *caps, uint64_t *exchange, int64_t bucket_cap);
+int tsdf_depth_window_update(tsdf_table *t, const uint64_t *received, int32_t world, int64_t bucket_cap,
+                             double sigma, double min_frac, double min_w, int32_t all_levels,
+                             tsdf_integration_stats *stats, tsdf_merge_stats *merge_stats);
+
+/* the CUDA stream every call of this table is ordered on (for callers that
+ * interleave their own work, e.g. collectives, with the table's) */
+int tsdf_table_stream(tsdf_table *t, void **stream);
+
 /* LiDAR hot-block update order (integrate_pointcloud, integrate.py:175-252).
  * TSDF_LIDAR_ORDERED (default): every voxel applies its observations in ray
  * order, the reference's _apply_batch arrival order (integrate.py:92-119):

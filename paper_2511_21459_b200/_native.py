@@ -87,6 +87,12 @@ def lib():
     L.tsdf_table_set_shard.argtypes = [_ptr, i32, i32]
     L.tsdf_table_set_depth_scale.argtypes = [_ptr, C.c_double]
     L.tsdf_table_set_lidar_mode.argtypes = [_ptr, i32]
+    L.tsdf_table_stream.argtypes = [_ptr, C.POINTER(_ptr)]
+    L.tsdf_depth_window_frames.argtypes = [_ptr, i32, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p, _f64p,
+                                           _f64p, dbl, dbl, i32, i32, _ptr]
+    L.tsdf_depth_window_walk.argtypes = [_ptr, _ptr, _ptr, i64]
+    L.tsdf_depth_window_update.argtypes = [_ptr, _ptr, i32, i64, dbl, dbl, dbl, i32, _ptr,
+                                           C.POINTER(MergeStatsC)]
     L.tsdf_table_merge_audit.argtypes = [_ptr, C.POINTER(C.c_int64)]
     L.tsdf_integrate_depth.argtypes = [_ptr, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p, _f64p,
                                        _f64p, dbl, dbl, C.POINTER(IntegrationStatsC)]

@@ -84,6 +84,12 @@ int tsdf_table_set_depth_scale(tsdf_table* t, double depth_scale) {
   return TSDF_OK;
 }
 
+int tsdf_table_stream(tsdf_table* t, void** stream) {
+  NEED(t);
+  *stream = (void*)T_(t)->stream;
+  return TSDF_OK;
+}
+
 int tsdf_table_set_lidar_mode(tsdf_table* t, int32_t mode) {
   NEED(t);
   if (mode != TSDF_LIDAR_ORDERED && mode != TSDF_LIDAR_CHUNKED) {
@@ -522,6 +528,54 @@ int tsdf_integrate_depth_window(tsdf_table* t, int32_t n_frames, const void* con
   }
   for (int i = 0; i < n_frames; i++) memcpy(&stats[i], &st[i], sizeof(st[i]));
   *n_done = done;
+  return s;
+}
+
+int tsdf_depth_window_frames(tsdf_table* t, int32_t n_frames, const void* const* depth,
+                             int32_t depth_dtype, const void* const* rgb, int32_t rgb_dtype,
+                             int32_t height, int32_t width, int32_t mem, const double* K,
+                             const double* R, const double* trans, double tau, double weight_cap,
+                             int32_t ray_rank, int32_t ray_world, uint64_t* caps) {
+  NEED(t);
+  if (n_frames <= 0) {
+    set_error("a window needs at least one frame");
+    return TSDF_EVALUE;
+  }
+  if (depth_dtype < 0 || depth_dtype > 3 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
+    set_error("unsupported dtype");
+    return TSDF_EVALUE;
+  }
+  std::vector<DepthArgs> args(n_frames);
+  for (int i = 0; i < n_frames; i++) {
+    if (K[4 * i] <= 0 || K[4 * i + 1] <= 0) {
+      set_error("focal lengths must be positive");
+      return TSDF_EDATASET;
+    }
+    args[i] = DepthArgs{depth[i], depth_dtype, rgb ? rgb[i] : nullptr, rgb_dtype, height, width,
+                        mem, make_frame(K + 4 * i, R + 9 * i, trans + 3 * i, tau, weight_cap)};
+  }
+  return depth_window_frames(T_(t), n_frames, args.data(), ray_rank, ray_world, caps);
+}
+
+int tsdf_depth_window_walk(tsdf_table* t, const uint64_t* caps, uint64_t* exchange, int64_t bucket_cap) {
+  NEED(t);
+  return depth_window_walk(T_(t), caps, exchange, bucket_cap);
+}
+
+int tsdf_depth_window_update(tsdf_table* t, const uint64_t* received, int32_t world, int64_t bucket_cap,
+                             double sigma, double min_frac, double min_w, int32_t all_levels,
+                             tsdf_integration_stats* stats, tsdf_merge_stats* merge_stats) {
+  NEED(t);
+  const int B = T_(t)->win.B;
+  std::vector<IntegrationStats> st(std::max(B, 1));
+  MergeArgs ma{sigma, min_frac, min_w, all_levels, 0.0};
+  MergeStats ms{0, 0};
+  int s = depth_window_update(T_(t), received, world, bucket_cap, &ma, st.data(), &ms);
+  for (int i = 0; i < B; i++) memcpy(&stats[i], &st[i], sizeof(st[i]));
+  if (merge_stats) {
+    merge_stats->candidates = ms.candidates;
+    merge_stats->merged = ms.merged;
+  }
   return s;
 }
 

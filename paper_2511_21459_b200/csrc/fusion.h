@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
 #include <map>
 #include <string>
 #include <vector>
@@ -32,6 +33,19 @@ struct Frame {
   double tau, weight_cap;
 };
 
+// a ray-sharded window between its three calls (fusion.cu "ray-sharded merge windows")
+struct WindowState {
+  int stage = 0;  // 1 after the frame passes, 2 after the walk
+  int B = 0, H = 0, W = 0, ray_rank = 0, ray_world = 1, depth_dtype = 0, rgb_dtype = 0;
+  int64_t cap = 0;
+  Counters* c = nullptr;
+  uint32_t* abort_word = nullptr;
+  std::vector<std::array<double, 24>> f;  // FrameDev images (fusion.cu)
+  std::vector<Frame> fr;
+  std::vector<const void*> dptr, cptr;  // device inputs of each frame
+  Buf depth, rgb, dray, pyr;            // staged inputs and per-frame scratch
+};
+
 struct Table {
   DevTable d{};
   uint32_t* free_top = nullptr;  // device [kMaxLevels]
@@ -46,12 +60,12 @@ struct Table {
   // synchronises; maintain_table() rebuilds the index once it passes slots/4
   unsigned long long* htomb = nullptr;
   uint64_t rehashes = 0;
-  size_t l2_window = 0;
+  size_t l2_window = 0;  // bytes of keys[] under the persisting L2 window (0: none)
   // LiDAR hot-segment mode: 0 = ordered (bit-exact ray order), 1 = chunked
   // (partial Welford states merged by Chan's formula; tsdf_table_set_lidar_mode)
   int lidar_mode = 0;
   // merge-pass audit: level decisions within 1e-6 relative of sigma so far
-  uint64_t merge_audit = 0;  // bytes of keys[] under the persisting L2 window (0: none)
+  uint64_t merge_audit = 0;
   uint32_t call_id = 0;
   double depth_scale = 1.0;  // raw u16 depth units per metre (tsdf_table_set_depth_scale)
   Buf mesh_out;                   // the last extract_mesh_begin result (device)
@@ -85,6 +99,7 @@ struct Table {
     double f[24];               // FrameDev image
   } shf;
   Frame shf_frame{};
+  WindowState win;
   Counters* hbatch = nullptr;  // pinned, hbatch_n entries
   int hbatch_n = 0;
   // work accounting for diagnostics: frames, touched, culled-in (depth
@@ -162,6 +177,11 @@ int integrate_depth_walk(Table* T, const DepthArgs& a, int ray_rank, int ray_wor
                          uint64_t* buckets, uint64_t bucket_cap, int64_t* counts,
                          IntegrationStats* st);
 int integrate_depth_keys(Table* T, const uint64_t* keys, int64_t n, IntegrationStats* st);
+int depth_window_frames(Table* T, int B, const DepthArgs* frames, int ray_rank, int ray_world,
+                        uint64_t* caps);
+int depth_window_walk(Table* T, const uint64_t* caps, uint64_t* exch, int64_t cap);
+int depth_window_update(Table* T, const uint64_t* recv, int world, int64_t cap, const MergeArgs* merge,
+                        IntegrationStats* st, MergeStats* mst);
 int depth_keys(Table* T, const DepthArgs& a, uint64_t* keys, int64_t cap, int64_t* n_out);
 int scan_keys(Table* T, const void* xyz, int xyz_dtype, int64_t n, int mem, const Frame& fr,
               uint64_t* keys, int64_t cap, int64_t* n_out);

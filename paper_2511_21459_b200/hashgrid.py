@@ -177,6 +177,13 @@ class HashTable:
             N.check(N.lib().tsdf_table_set_depth_scale(self._h, depth_scale), "set_depth_scale")
             self._depth_scale = depth_scale
 
+    @property
+    def cuda_stream(self) -> int:
+        """The cudaStream_t (as an int) every call of this table is ordered on."""
+        out = C.c_void_p()
+        N.check(N.lib().tsdf_table_stream(self._h, C.byref(out)), "cuda_stream")
+        return int(out.value or 0)
+
     def set_lidar_mode(self, mode: str) -> None:
         """LiDAR hot-block update order: "ordered" (default; bit-identical to
         the reference's ray-order Welford chain) or "chunked" (observations

@@ -244,11 +244,10 @@ def integrate_depth_window(table: HashTable, frames, tau: float, sigma_threshold
     return st, ms
 
 
-def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial=False):
-    """-> (stats of the frames applied, MergeStats, frames applied); with
-    partial=True a failing frame does not raise: its error is returned as a
-    fourth element (None if every frame was applied or the fill mark stopped
-    the window)."""
+def _window_args(table, frames):
+    """The C-ABI view of a window of depth frames: (keep-alive list, depth
+    pointer array, depth dtype, colour pointer array or None, colour dtype,
+    memory kind, H, W, K, R, t)."""
     n = len(frames)
     keep, dptrs, cptrs = [], [], []
     ddt = cdt = mem = None
@@ -278,11 +277,21 @@ def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial
     T = np.concatenate([f.pose.translation for f in frames])
     darr = (C.c_void_p * n)(*dptrs)
     carr = (C.c_void_p * n)(*cptrs) if cptrs else None
+    return keep, darr, ddt, carr, cdt or 0, mem, H, W, K, R, T
+
+
+def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial=False):
+    """-> (stats of the frames applied, MergeStats, frames applied); with
+    partial=True a failing frame does not raise: its error is returned as a
+    fourth element (None if every frame was applied or the fill mark stopped
+    the window)."""
+    n = len(frames)
+    keep, darr, ddt, carr, cdt, mem, H, W, K, R, T = _window_args(table, frames)
     st = (N.IntegrationStatsC * n)()
     done = C.c_int32()
     ms = N.MergeStatsC()
     sig, frac, minw, alll = merge if merge is not None else (0.0, 0.0, 0.0, False)
-    rc = N.lib().tsdf_integrate_depth_window(table._h, n, darr, ddt, carr, cdt or 0,
+    rc = N.lib().tsdf_integrate_depth_window(table._h, n, darr, ddt, carr, cdt,
                                              H, W, mem, K, R, T,
                                              float(tau), float(weight_cap), st, C.byref(done),
                                              float(sig), float(frac), float(minw), int(bool(alll)),
@@ -301,6 +310,58 @@ def _depth_window(table, frames, tau, weight_cap, merge, fill_limit=0.0, partial
     return out + (None,) if partial else out
 
 
+
+
+# ---- ray-sharded merge windows (sharding.integrate_depth_window_sharded) ----
+
+def _cuda_ptr(a, what, n_min=1):
+    cai = getattr(a, "__cuda_array_interface__", None)
+    if cai is None or np.dtype(cai["typestr"]).itemsize != 8 or int(np.prod(cai["shape"])) < n_min:
+        raise ValueError(f"{what} must be a 64-bit CUDA array of at least {n_min} elements")
+    return cai["data"][0]
+
+
+def depth_window_frames(table: HashTable, frames, tau: float, ray_rank: int, ray_world: int, caps,
+                        weight_cap: float = 0.0):
+    """Window step 1 (include/tsdf_b200.h tsdf_depth_window_frames): the
+    frames' pixel passes, this rank's partial lock-step caps into `caps`
+    (CUDA u64/i64 [B]).  The frames must stay alive until the update step."""
+    if tau <= 0:
+        raise ValueError("tau must be positive")
+    frames = list(frames)
+    keep, darr, ddt, carr, cdt, mem, H, W, K, R, T = _window_args(table, frames)
+    table._win_keep = (frames, keep, darr, carr)
+    N.check(N.lib().tsdf_depth_window_frames(table._h, len(frames), darr, ddt, carr, cdt, H, W, mem, K, R, T,
+                                             float(tau), float(weight_cap), int(ray_rank), int(ray_world),
+                                             _cuda_ptr(caps, "caps", len(frames))),
+            "depth_window_frames")
+
+
+def depth_window_walk(table: HashTable, caps, exchange, bucket_cap: int):
+    """Window step 2: walk this rank's rays with the all-reduced caps and fill
+    the exchange buffer (CUDA 64-bit, shard_world * B * (bucket_cap + 1))."""
+    N.check(N.lib().tsdf_depth_window_walk(table._h, _cuda_ptr(caps, "caps"), _cuda_ptr(exchange, "exchange"),
+                                           int(bucket_cap)), "depth_window_walk")
+
+
+def depth_window_update(table: HashTable, received, world: int, bucket_cap: int, n_frames: int,
+                        sigma_threshold: float = 0.0, min_eligible_fraction: float = 0.05,
+                        min_mean_weight: float = 3.0, all_levels: bool = False):
+    """Window step 3: insert / commit / update every frame from the exchanged
+    keys, then one merge pass (sigma_threshold > 0).  Returns (this shard's
+    per-frame stats, MergeStats)."""
+    from .adapt import MergeStats
+    st = (N.IntegrationStatsC * n_frames)()
+    ms = N.MergeStatsC()
+    try:
+        N.check(N.lib().tsdf_depth_window_update(table._h, _cuda_ptr(received, "received"), int(world),
+                                                 int(bucket_cap), float(sigma_threshold),
+                                                 float(min_eligible_fraction), float(min_mean_weight),
+                                                 int(bool(all_levels)), st, C.byref(ms)),
+                "depth_window_update")
+    finally:
+        table._win_keep = None
+    return [_stats(x) for x in st], MergeStats(int(ms.candidates), int(ms.merged))
 
 
 def integrate_pointcloud(table: HashTable, frame: PointCloudFrame, tau: float, archive=None,

@@ -564,3 +564,138 @@ def extract_mesh_halo_local(tables, iso: float = 0.0, collapse_epsilon=None):
               for d in range(world)] for o in range(world)]
     raws = [_mesh_slab(tables[r], plan, r, [sends[o][r] for o in range(world)], iso) for r in range(world)]
     return finish_raw([_raw_from_bytes(b) for b in raws], tables[0].block_edge, collapse_epsilon), plan
+
+
+# ---------------------------------------------------------------------------
+# Ray-sharded merge windows (the multi-GPU split of a window of
+# pipeline.py:88-137).  Per window of B frames: the pixel passes (span for
+# the lock-step cap split by tile) -> all-reduce MAX of B caps -> the walks of
+# this rank's rays of all B frames -> one all-to-all of the per-(owner,
+# frame) key buckets -> inserts, commits and voxel updates frame by frame ->
+# one merge pass -> one all-reduce of the per-frame counters.  The library
+# and the collectives are ordered through CUDA events (no host wait) except
+# for one small read of the bucket counts per window (sizes the exchange) and
+# the final counters.  Frame order per block is unchanged, so the union of
+# the shards equals the single-GPU window bit for bit.
+# ---------------------------------------------------------------------------
+
+def _torch_waits_for_table(table, torch):
+    s = table.cuda_stream
+    if s:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(s))
+        torch.cuda.current_stream().wait_event(ev)
+
+
+def _table_waits_for_torch(table, torch):
+    s = table.cuda_stream
+    if s:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        torch.cuda.ExternalStream(s).wait_event(ev)
+
+
+def _window_cap(table, counts_max: int) -> int:
+    return max(4096, -(-int(counts_max * 5 // 4 + 64) // 1024) * 1024)
+
+
+def integrate_depth_window_sharded(table, frames, tau, dist, torch, group=None, device=None,
+                                   sigma_threshold: float = 0.0, min_eligible_fraction: float = 0.05,
+                                   min_mean_weight: float = 3.0, all_levels: bool = False,
+                                   weight_cap: float = 0.0):
+    """One merge window on this rank's shard (see above).  Returns (per-frame
+    IntegrationStats summed over ranks, MergeStats summed over ranks)."""
+    from .adapt import MergeStats
+    from .integrate import (IntegrationStats, depth_window_frames, depth_window_update,
+                            depth_window_walk)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    gloo = dist.get_backend(group) == "gloo"
+    frames = list(frames)
+    B = len(frames)
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    caps = torch.zeros(B, dtype=torch.int64, device=dev)
+    depth_window_frames(table, frames, tau, rank, world, caps, weight_cap)
+    _torch_waits_for_table(table, torch)
+    if gloo:
+        hc = caps.cpu()
+        dist.all_reduce(hc, op=dist.ReduceOp.MAX, group=group)
+        caps.copy_(hc)
+    else:
+        dist.all_reduce(caps, op=dist.ReduceOp.MAX, group=group)
+    _table_waits_for_torch(table, torch)
+    cap = getattr(table, "_win_cap", 8192)
+    for _ in range(3):
+        stride = B * (cap + 1)
+        exch = torch.empty(world * stride, dtype=torch.int64, device=dev)
+        depth_window_walk(table, caps, exch, cap)
+        _torch_waits_for_table(table, torch)
+        # the largest bucket of the window, over every rank (one small read)
+        mx = exch.view(world, stride)[:, :B].max().reshape(1)
+        mx = mx.cpu() if gloo else mx
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        need = int(mx.item())
+        table._win_cap = _window_cap(table, need)
+        if need <= cap:
+            break
+        cap = table._win_cap  # re-walk with room (the walk changes nothing)
+        table._win_rewalks = getattr(table, "_win_rewalks", 0) + 1
+    if gloo:
+        send = exch.cpu()
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=group)
+        recv = recv.to(dev)
+        torch.cuda.current_stream().synchronize()
+    else:
+        recv = torch.empty_like(exch)
+        dist.all_to_all_single(recv, exch, group=group)
+    _table_waits_for_torch(table, torch)
+    st, ms = depth_window_update(table, recv, world, cap, B, sigma_threshold, min_eligible_fraction,
+                                 min_mean_weight, all_levels)
+    v = torch.tensor([[getattr(s, k) for k in PARTITIONED] for s in st] + [[ms.candidates, ms.merged, 0, 0]],
+                     dtype=torch.int64, device="cpu" if gloo else dev)
+    dist.all_reduce(v, group=group)
+    v = v.cpu().tolist()
+    out = []
+    for s, row in zip(st, v[:B]):
+        o = IntegrationStats(**{k: getattr(s, k) for k in INVARIANT})
+        for k, x in zip(PARTITIONED, row):
+            setattr(o, k, int(x))
+        o.warnings = list(s.warnings)
+        out.append(o)
+    return out, MergeStats(int(v[B][0]), int(v[B][1]))
+
+
+def integrate_depth_window_local(tables, frames, tau, sigma_threshold: float = 0.0,
+                                 all_levels: bool = False, weight_cap: float = 0.0, bucket_cap=None):
+    """The same window protocol over shard tables living in one process (the
+    collectives replaced by tensor plumbing): the single-GPU test of
+    integrate_depth_window_sharded, step for step."""
+    import torch
+    from .adapt import MergeStats
+    from .integrate import (IntegrationStats, depth_window_frames, depth_window_update,
+                            depth_window_walk)
+    world, B = len(tables), len(frames)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    caps = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(world)]
+    for r, t in enumerate(tables):
+        depth_window_frames(t, frames, tau, r, world, caps[r], weight_cap)
+    torch.cuda.synchronize()
+    cap_all = torch.stack(caps).max(0).values.contiguous()
+    cap = bucket_cap or 8192
+    stride = B * (cap + 1)
+    exch = [torch.empty(world * stride, dtype=torch.int64, device=dev) for _ in range(world)]
+    for r, t in enumerate(tables):
+        depth_window_walk(t, cap_all, exch[r], cap)
+    torch.cuda.synchronize()
+    need = max(int(e.view(world, stride)[:, :B].max()) for e in exch)
+    recv = [torch.cat([exch[s].view(world, stride)[r] for s in range(world)]).contiguous()
+            for r in range(world)]
+    res = [depth_window_update(t, recv[r], world, cap, B, sigma_threshold, all_levels=all_levels)
+           for r, t in enumerate(tables)]
+    out = []
+    for i in range(B):
+        o = IntegrationStats(**{k: getattr(res[0][0][i], k) for k in INVARIANT})
+        for k in PARTITIONED:
+            setattr(o, k, sum(getattr(r[0][i], k) for r in res))
+        out.append(o)
+    return out, MergeStats(sum(r[1].candidates for r in res), sum(r[1].merged for r in res)), need

@@ -260,7 +260,7 @@ def test_capacity_error_parity_with_oracle():
 
 def test_frame_capacity_error_rolls_back():
     import paper_2511_21459_b200 as P
-    f = P.synth.render_frames("room", 1, 64, 48)[0]
+    f = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 1, 64, 48)[0]
     t = P.HashTable(100003, 10, 7, 0.08, (50, 10))
     with pytest.raises(P.CapacityError):
         P.integrate_depth(t, f, 0.03)
@@ -280,7 +280,7 @@ def test_deterministic_rerun_bit_identical():
 def test_device_resident_inputs_match_host_inputs():
     torch = pytest.importorskip("torch")
     import paper_2511_21459_b200 as P
-    frames = P.synth.render_frames("room", 3, 160, 120, depth_dtype=np.float32,
+    frames = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 3, 160, 120, depth_dtype=np.float32,
                                    color_dtype=np.uint8)
     a = P.HashTable(1000003, 10, 7, 0.04, (60000, 1000))
     b = P.HashTable(1000003, 10, 7, 0.04, (60000, 1000))
@@ -312,7 +312,7 @@ def test_block_key_sharding_union_equals_single_gpu(world):
     table bit-for-bit and the partitioned counters sum to its counters."""
     import paper_2511_21459_b200 as P
     from paper_2511_21459_b200.sharding import INVARIANT, PARTITIONED, owner_of_coords
-    frames = P.synth.render_frames("room", 20, 160, 120, depth_dtype=np.float32,
+    frames = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 20, 160, 120, depth_dtype=np.float32,
                                    color_dtype=np.uint8)
     full = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000))
     shards = []
@@ -356,7 +356,7 @@ def test_ray_sharded_allocation_union_equals_single_gpu(world):
     import torch
     import paper_2511_21459_b200 as P
     from paper_2511_21459_b200.sharding import INVARIANT, PARTITIONED, owner_of_coords
-    frames = P.synth.render_frames("room", 20, 160, 120, depth_dtype=np.float32,
+    frames = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 20, 160, 120, depth_dtype=np.float32,
                                    color_dtype=np.uint8)
     full = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000))
     shards = []
@@ -410,7 +410,7 @@ def test_ray_sharded_keys_need_walk_and_routing():
     dev = torch.device("cuda", 0)
     with pytest.raises(ValueError):
         P.integrate_depth_keys(t, torch.zeros(1, dtype=torch.int64, device=dev))
-    f = P.synth.render_frames("room", 1, 64, 48, depth_dtype=np.float32)[0]
+    f = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 1, 64, 48, depth_dtype=np.float32)[0]
     b = torch.zeros((2, t.slots), dtype=torch.int64, device=dev)
     P.integrate_depth_walk(t, f, 0.015, 0, 1, b)
     coords = np.array([[i, 0, 0] for i in range(64)])
@@ -425,7 +425,7 @@ def test_depth_window_equals_batch_then_merge(all_levels):
     """integrate_depth_window (frames + merge pass, one host sync) ==
     integrate_depth_batch followed by apply_merges, window after window."""
     import paper_2511_21459_b200 as P
-    frames = P.synth.render_frames("room", 30, 160, 120, depth_dtype=np.float32,
+    frames = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 30, 160, 120, depth_dtype=np.float32,
                                    color_dtype=np.uint8)
     caps = (100000, 20000, 5000)
     a = P.HashTable(1000003, 10, 7, 0.04, caps)
@@ -458,7 +458,7 @@ def test_merge_heap_exhaustion_changes_nothing():
 def test_depth_batch_equals_per_frame_and_oracle():
     """integrate_depth_batch (one host sync per merge window) == per-frame calls == oracle."""
     import paper_2511_21459_b200 as P
-    frames = P.synth.render_frames("room", 20, 160, 120, depth_dtype=np.float32,
+    frames = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 20, 160, 120, depth_dtype=np.float32,
                                    color_dtype=np.uint8)
     a = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000, 5000))
     b = P.HashTable(1000003, 10, 7, 0.04, (100000, 20000, 5000))
@@ -480,7 +480,7 @@ def test_depth_batch_equals_per_frame_and_oracle():
 
 def test_depth_batch_capacity_error_stops_at_failing_frame():
     import paper_2511_21459_b200 as P
-    frames = P.synth.render_frames("room", 4, 64, 48)
+    frames = __import__("paper_2511_21459_b200.synth", fromlist=["x"]).render_frames("room", 4, 64, 48)
     t = P.HashTable(100003, 10, 7, 0.08, (700, 10))
     single = P.HashTable(100003, 10, 7, 0.08, (700, 10))
     n_ok = 0
@@ -660,3 +660,42 @@ def test_halo_extraction_equals_single_gpu(world):
     # each rank moved its slab + halo, not the map
     need = sum(len(n) for n in plan["need"])
     assert need < 2.0 * full.live_count()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_window_union_equals_single_gpu(world):
+    """Ray-sharded merge windows (integrate_depth_window_sharded
+    with its collectives as tensor plumbing): the pixel passes split the
+    lock-step span by tile, the caps are max-reduced, every shard walks its
+    rays of all frames, one exchange routes the keys, each shard inserts and
+    updates frame by frame and merges -- the union equals the single-GPU
+    window bit for bit, with identical per-frame stats and merge counts."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    from paper_2511_21459_b200.sharding import integrate_depth_window_local
+    frames = synth.render_frames("room", 20, 128, 96, depth_dtype=np.float32, color_dtype=np.uint8)
+    caps = (100000, 20000, 5000)
+    full = P.HashTable(1000003, 10, 7, 0.04, caps)
+    shards = []
+    for r in range(world):
+        t = P.HashTable(1000003, 10, 7, 0.04, caps)
+        t.set_shard(r, world)
+        shards.append(t)
+    for w0 in (0, 10):
+        win = frames[w0:w0 + 10]
+        sf, mf = P.integrate_depth_window(full, win, 0.015, 2.5e-5, all_levels=True)
+        ss, ms, need = integrate_depth_window_local(shards, win, 0.015, 2.5e-5, all_levels=True,
+                                                    bucket_cap=200000)
+        assert need <= 200000
+        keys = PU.STAT_KEYS
+        assert [{k: getattr(s, k) for k in keys} for s in ss] == [{k: getattr(s, k) for k in keys} for s in sf]
+        assert (ms.candidates, ms.merged) == (mf.candidates, mf.merged)
+    assert full.heaps[1].occupied > 0
+    for l in range(full.num_levels):
+        ref = full.export_level(l)
+        parts = [s.export_level(l) for s in shards]
+        uc = np.concatenate([p[0] for p in parts])
+        order = np.lexsort((uc[:, 2], uc[:, 1], uc[:, 0]))
+        assert np.array_equal(uc[order], ref[0])
+        for i in (2, 3, 4, 5):
+            assert np.array_equal(np.concatenate([p[i] for p in parts])[order], ref[i])
