@@ -252,12 +252,20 @@ def window(P, t, wl, frs, dev=None):
 
 
 def window_and_merge(P, t, wl, frs, dev=None):
-    """One step: a merge window plus its merge pass.  Single-GPU depth
-    windows go through integrate_depth_window (frames + merge pass enqueued
-    together, one host synchronisation); otherwise window() + apply_merges."""
-    if wl["kind"] == "depth" and not _MULTI:
+    """One step: a merge window plus its merge pass.  Depth windows go
+    through integrate_depth_window (frames + merge pass enqueued together,
+    one host synchronisation) or, on N GPUs, integrate_depth_window_sharded;
+    scans through window() + apply_merges."""
+    if wl["kind"] == "depth":
         fs = [P.DepthFrame(depth=fr[0] if dev is None else dev[i][0], intrinsics=fr[3], pose=fr[2],
                            color=fr[1] if dev is None else dev[i][1]) for i, fr in enumerate(frs)]
+        if _MULTI:
+            # ray-sharded merge window: 3 collectives per window, no per-frame host sync
+            from paper_2511_21459_b200.sharding import integrate_depth_window_sharded
+            stats, ms = integrate_depth_window_sharded(t, fs, wl["tau"], _MULTI["dist"], _MULTI["torch"],
+                                                       device=_MULTI["device"], sigma_threshold=wl["sigma"],
+                                                       all_levels=True)
+            return stats, ms.merged
         stats, ms = P.integrate_depth_window(t, fs, wl["tau"], wl["sigma"], all_levels=True)
         return stats, ms.merged
     stats = window(P, t, wl, frs, dev)
@@ -360,20 +368,31 @@ def run_b200(name, W, K, rank, world, dist, torch, frames=None):
     extract = None
     if wl["kind"] == "depth":
         eps = 0.25 * wl["edge"] / 8
-        P.extract_mesh(table, 0.0, eps)
+        if world > 1:
+            # the whole map's mesh from the shards: spatial chunk runs + halo
+            from paper_2511_21459_b200.sharding import extract_mesh_halo
+            run = lambda: extract_mesh_halo(table, dist, torch, device=dev, collapse_epsilon=eps)  # noqa: E731
+            how = "sharding.extract_mesh_halo over the shards (mesh on rank 0), wall clock"
+        else:
+            run = lambda: P.extract_mesh(table, 0.0, eps)  # noqa: E731
+            how = "public extract_mesh on the final map, wall clock incl. D2H of the mesh"
+        run()
         table.kernel_times(reset=True)
         table.profile(True)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        mesh = P.extract_mesh(table, 0.0, eps)
+        mesh = run()
         ex_s = time.perf_counter() - t0
         mk = table.kernel_times(reset=True)
         table.profile(False)
-        extract = {"ms": round(ex_s * 1e3, 3), "vertices": int(mesh.num_vertices),
-                   "triangles": int(mesh.num_triangles),
-                   "mtriangles_per_s": round(mesh.num_triangles / ex_s / 1e6, 3),
-                   "kernels_ms": {k: round(v[0], 3) for k, v in sorted(mk.items(), key=lambda kv: -kv[1][0])[:6]},
-                   "note": "public extract_mesh on the final map, wall clock incl. D2H of the mesh"}
+        if mesh is not None:
+            extract = {"ms": round(ex_s * 1e3, 3), "vertices": int(mesh.num_vertices),
+                       "triangles": int(mesh.num_triangles),
+                       "mtriangles_per_s": round(mesh.num_triangles / ex_s / 1e6, 3),
+                       "kernels_ms": {k: round(v[0], 3) for k, v in sorted(mk.items(), key=lambda kv: -kv[1][0])[:6]},
+                       "note": how}
     dev_ms = float(sum(step_ms))
     if world > 1:
         tt = torch.tensor([dev_ms], dtype=torch.float64, device=dev)

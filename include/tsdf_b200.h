@@ -302,6 +302,11 @@ int tsdf_scan_keys(tsdf_table *t, const void *xyz, int32_t xyz_dtype, int64_t n,
  * exhaustion; either way the table is left as before the call). */
 int tsdf_evict_level(tsdf_table *t, int32_t level, const int64_t *coords, int64_t n, double *tsdf,
                      double *weight, double *s2, float *color);
+/* the payloads of live blocks of one level given as packed keys, the table
+ * unchanged (evict's gather without the removal; TSDF_ENOTFOUND if one is
+ * not live at that level) */
+int tsdf_read_level_blocks(tsdf_table *t, int32_t level, const uint64_t *keys, int64_t n, double *tsdf,
+                           double *weight, double *s2, float *color);
 int tsdf_import_level(tsdf_table *t, int32_t level, const int64_t *coords, int64_t n,
                       const double *tsdf, const double *weight, const double *s2,
                       const float *color);

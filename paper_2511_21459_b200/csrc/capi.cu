@@ -203,6 +203,12 @@ int tsdf_evict_level(tsdf_table* t, int32_t level, const int64_t* coords, int64_
   return evict_blocks(T_(t), level, coords, n, tsdf, weight, s2, color);
 }
 
+int tsdf_read_level_blocks(tsdf_table* t, int32_t level, const uint64_t* keys, int64_t n, double* tsdf,
+                           double* weight, double* s2, float* color) {
+  NEED(t);
+  return read_blocks(T_(t), level, keys, n, tsdf, weight, s2, color);
+}
+
 int tsdf_import_level(tsdf_table* t, int32_t level, const int64_t* coords, int64_t n,
                       const double* tsdf, const double* weight, const double* s2,
                       const float* color) {

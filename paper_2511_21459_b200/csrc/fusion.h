@@ -232,6 +232,8 @@ int extract_mesh(Table* T, double iso, double eps, MeshOut* out);
 int extract_mesh_begin(Table* T, double iso, double eps, int64_t* nv, int64_t* nt);
 int extract_mesh_read(Table* T, double* v, double* n, double* c, int64_t* tri);
 void mesh_free(MeshOut* m);
+int read_blocks(Table* T, int32_t level, const uint64_t* keys, int64_t n, double* tsdf, double* weight,
+                double* s2, float* color);
 int mesh_block_summary(Table* T, uint64_t* keys, int32_t* levels, uint8_t* obs, double* lo,
                        double* hi, int64_t cap, int64_t* n_out);
 int mesh_emit_keys(Table* T, const uint64_t* keys, const int64_t* level_counts, double iso,

@@ -371,6 +371,20 @@ class HashTable:
                     "evict")
         return t, w, s2, col
 
+    def read_blocks(self, level: int, keys):
+        """Payloads (tsdf, weight, s2 f64 [n, nvox]; color f32 [n, nvox, 3])
+        of live blocks of one level given as packed keys; the table is
+        unchanged (NotFoundError if one is not live at that level)."""
+        k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1))
+        n, nvox = len(k), self.heaps[level].nvox
+        t, w, s2 = (np.zeros((n, nvox)) for _ in range(3))
+        col = np.zeros((n, nvox, 3), dtype=np.float32)
+        if n:
+            N.check(N.lib().tsdf_read_level_blocks(self._h, int(level), k.ctypes.data, n, t.ctypes.data,
+                                                   w.ctypes.data, s2.ctypes.data, col.ctypes.data),
+                    "read_blocks")
+        return t, w, s2, col
+
     def import_blocks(self, level: int, coords, tsdf, weight, s2, color) -> None:
         """Insert blocks at `level` with their payloads (the inverse of
         evict).  All or nothing: ValueError if one is already live,

@@ -77,6 +77,23 @@ class ShardedFusion:
         st = self.engine.integrate_frame(f)
         return combine_stats(st, self.dist, self.torch, self.group, self.device)
 
+    def integrate_window(self, frames, merge: bool = True):
+        """A merge window of depth frames (rank 0's frames; every rank passes
+        a list of the same length) through the ray-sharded window protocol:
+        the frames, then (merge) the merge pass, with three collectives and
+        one host synchronisation per window.  Returns (per-frame stats,
+        merged blocks), summed over ranks."""
+        frames = [self.broadcast_frame(f) if self.world > 1 else f for f in frames]
+        cfg = self.engine.config
+        st, ms = integrate_depth_window_sharded(
+            self.engine.table, frames, cfg.tau, self.dist, self.torch, self.group, self.device,
+            sigma_threshold=cfg.sigma_threshold if merge else 0.0,
+            min_eligible_fraction=cfg.merge_min_eligible_fraction,
+            min_mean_weight=cfg.merge_min_mean_weight, all_levels=cfg.merge_all_levels,
+            weight_cap=cfg.weight_cap)
+        self.engine.frame_index += len(frames)
+        return st, ms.merged
+
     def extract(self, iso: float = 0.0, dst: int = 0):
         """FusionEngine.extract over the whole map: the mesh on rank `dst`
         (None elsewhere)."""
@@ -423,18 +440,27 @@ def mesh_plan(summaries, world: int, iso: float = 0.0, n_levels: int = 2) -> dic
     return {"emit": emit, "need": need, "kept": int(total), "chunks": len(chunks), "bounds": bounds}
 
 
-def _records_for(table, keys) -> bytes:
-    """shard_records restricted to the given packed keys."""
+def _records_for(table, keys, levels) -> bytes:
+    """shard_records restricted to the given packed keys (with their levels):
+    one device gather per level, the table unchanged."""
     from .formats import pack_records
     counts, out = [], []
-    want = np.asarray(keys, dtype=np.uint64)
+    keys = np.asarray(keys, dtype=np.uint64)
+    levels = np.asarray(levels)
     for level in range(table.num_levels):
-        coords, _, t, w, s2, col = table.export_level(level)
-        sel = np.isin(pack_keys(coords), want) if len(coords) else np.zeros(0, bool)
-        counts.append(int(sel.sum()))
-        if counts[-1]:
-            out.append(pack_records(level, coords[sel], t[sel], w[sel], s2[sel], col[sel]).tobytes())
+        k = np.sort(keys[levels == level])
+        counts.append(len(k))
+        if len(k):
+            t, w, s2, col = table.read_blocks(level, k)
+            out.append(pack_records(level, unpack_keys(k), t, w, s2, col).tobytes())
     return np.asarray([table.num_levels] + counts, dtype="<u8").tobytes() + b"".join(out)
+
+
+def _owned_need(summary, need):
+    """(keys, levels) of this rank's blocks among `need` (sorted packed keys)."""
+    k = np.asarray(summary["keys"], dtype=np.uint64)
+    sel = np.isin(k, need)
+    return k[sel], np.asarray(summary["levels"])[sel]
 
 
 def _raw_bytes(m) -> bytes:
@@ -541,8 +567,7 @@ def extract_mesh_halo(table, dist, torch, group=None, device=None, iso: float = 
     summ = [_summary_from_bytes(b) for b in
             _all_gather_bytes(_summary_bytes(block_summary(table)), dist, torch, group, device)]
     plan = mesh_plan(summ, world, iso, table.num_levels)
-    mine = set(summ[rank]["keys"].tolist())
-    sends = [_records_for(table, [k for k in plan["need"][d].tolist() if k in mine]) for d in range(world)]
+    sends = [_records_for(table, *_owned_need(summ[rank], plan["need"][d])) for d in range(world)]
     blobs = all_to_all_bytes(sends, dist, torch, group, device)
     raw = _mesh_slab(table, plan, rank, blobs, iso)
     raws = _gather_bytes(raw, dst, dist, torch, group, device)
@@ -559,9 +584,8 @@ def extract_mesh_halo_local(tables, iso: float = 0.0, collapse_epsilon=None):
     world = len(tables)
     summ = [block_summary(t) for t in tables]
     plan = mesh_plan(summ, world, iso, tables[0].num_levels)
-    owned = [set(s["keys"].tolist()) for s in summ]
-    sends = [[_records_for(tables[o], [k for k in plan["need"][d].tolist() if k in owned[o]])
-              for d in range(world)] for o in range(world)]
+    sends = [[_records_for(tables[o], *_owned_need(summ[o], plan["need"][d])) for d in range(world)]
+             for o in range(world)]
     raws = [_mesh_slab(tables[r], plan, r, [sends[o][r] for o in range(world)], iso) for r in range(world)]
     return finish_raw([_raw_from_bytes(b) for b in raws], tables[0].block_edge, collapse_epsilon), plan
 
