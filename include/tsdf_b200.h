@@ -126,6 +126,9 @@ int tsdf_depth_window_update(tsdf_table *t, const uint64_t *received, int32_t wo
 /* the CUDA stream every call of this table is ordered on (for callers that
  * interleave their own work, e.g. collectives, with the table's) */
 int tsdf_table_stream(tsdf_table *t, void **stream);
+/* a counter bumped by every call that can change the map (host caches of
+ * heap contents, e.g. BlockHeap.tsdf, are valid while it is unchanged) */
+int tsdf_table_version(tsdf_table *t, uint64_t *version);
 
 /* LiDAR hot-block update order (integrate_pointcloud, integrate.py:175-252).
  * TSDF_LIDAR_ORDERED (default): every voxel applies its observations in ray

@@ -88,6 +88,7 @@ def lib():
     L.tsdf_table_set_depth_scale.argtypes = [_ptr, C.c_double]
     L.tsdf_table_set_lidar_mode.argtypes = [_ptr, i32]
     L.tsdf_table_stream.argtypes = [_ptr, C.POINTER(_ptr)]
+    L.tsdf_table_version.argtypes = [_ptr, C.POINTER(C.c_uint64)]
     L.tsdf_read_level_blocks.argtypes = [_ptr, i32, _ptr, i64, _ptr, _ptr, _ptr, _ptr]
     L.tsdf_depth_window_frames.argtypes = [_ptr, i32, _ptr, i32, _ptr, i32, i32, i32, i32, _f64p, _f64p,
                                            _f64p, dbl, dbl, i32, i32, _ptr]

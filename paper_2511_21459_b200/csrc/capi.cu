@@ -60,6 +60,7 @@ int tsdf_table_destroy(tsdf_table* t) {
 
 int tsdf_table_reset(tsdf_table* t) {
   NEED(t);
+  T_(t)->version++;
   return table_reset(T_(t));
 }
 
@@ -81,6 +82,12 @@ int tsdf_table_set_depth_scale(tsdf_table* t, double depth_scale) {
     return TSDF_EVALUE;
   }
   T_(t)->depth_scale = depth_scale;
+  return TSDF_OK;
+}
+
+int tsdf_table_version(tsdf_table* t, uint64_t* version) {
+  NEED(t);
+  *version = T_(t)->version;
   return TSDF_OK;
 }
 
@@ -111,6 +118,7 @@ int tsdf_integrate_depth(tsdf_table* t, const void* depth, int32_t depth_dtype, 
                          const double* K, const double* R, const double* trans, double tau,
                          double weight_cap, tsdf_integration_stats* stats) {
   NEED(t);
+  T_(t)->version++;
   if (depth_dtype < 0 || depth_dtype > 3 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
     set_error("unsupported dtype");
     return TSDF_EVALUE;
@@ -157,6 +165,7 @@ int tsdf_integrate_depth_walk(tsdf_table* t, const void* depth, int32_t depth_dt
 int tsdf_integrate_depth_keys(tsdf_table* t, const uint64_t* keys, int64_t n,
                               tsdf_integration_stats* stats) {
   NEED(t);
+  T_(t)->version++;
   if (n < 0 || (n > 0 && !keys)) {
     set_error("invalid key list");
     return TSDF_EVALUE;
@@ -200,6 +209,7 @@ int tsdf_scan_keys(tsdf_table* t, const void* xyz, int32_t xyz_dtype, int64_t n,
 int tsdf_evict_level(tsdf_table* t, int32_t level, const int64_t* coords, int64_t n, double* tsdf,
                      double* weight, double* s2, float* color) {
   NEED(t);
+  T_(t)->version++;
   return evict_blocks(T_(t), level, coords, n, tsdf, weight, s2, color);
 }
 
@@ -213,6 +223,7 @@ int tsdf_import_level(tsdf_table* t, int32_t level, const int64_t* coords, int64
                       const double* tsdf, const double* weight, const double* s2,
                       const float* color) {
   NEED(t);
+  T_(t)->version++;
   return import_blocks(T_(t), level, coords, n, tsdf, weight, s2, color);
 }
 
@@ -221,6 +232,7 @@ int tsdf_integrate_points(tsdf_table* t, const void* xyz, int32_t xyz_dtype, con
                           const double* trans, double tau, double weight_cap,
                           tsdf_integration_stats* stats) {
   NEED(t);
+  T_(t)->version++;
   if (xyz_dtype < 0 || xyz_dtype > 1 || (rgb && (rgb_dtype < 0 || rgb_dtype > 2))) {
     set_error("unsupported dtype");
     return TSDF_EVALUE;
@@ -235,12 +247,14 @@ int tsdf_integrate_points(tsdf_table* t, const void* xyz, int32_t xyz_dtype, con
 int tsdf_allocate_for_measurement(tsdf_table* t, const double* origin, const double* p,
                                   double tau, int64_t* handles, int64_t max_out, int64_t* n_out) {
   NEED(t);
+  T_(t)->version++;
   return allocate_for_measurement(T_(t), origin, p, tau, handles, max_out, n_out);
 }
 
 int tsdf_apply_merges(tsdf_table* t, double sigma, double min_frac, double min_w,
                       int32_t all_levels, tsdf_merge_stats* stats) {
   NEED(t);
+  T_(t)->version++;
   MergeStats st;
   int s = apply_merges(T_(t), sigma, min_frac, min_w, all_levels, &st);
   stats->candidates = st.candidates;
@@ -326,12 +340,14 @@ int tsdf_find_batch(tsdf_table* t, const int64_t* coords, int64_t n, int64_t* ha
 
 int tsdf_insert(tsdf_table* t, const int64_t* coord, int32_t level, int64_t* handle) {
   NEED(t);
+  T_(t)->version++;
   return insert_block(T_(t), coord, level, handle);
 }
 
 int tsdf_remove(tsdf_table* t, const int64_t* coord, int32_t* level, double* tsdf,
                 double* weight, double* s2, float* color) {
   NEED(t);
+  T_(t)->version++;
   return remove_block(T_(t), coord, level, tsdf, weight, s2, color);
 }
 
@@ -344,6 +360,7 @@ int tsdf_read_block(tsdf_table* t, const int64_t* coord, int32_t* level, double*
 int tsdf_write_block(tsdf_table* t, const int64_t* coord, const double* tsdf,
                      const double* weight, const double* s2, const float* color) {
   NEED(t);
+  T_(t)->version++;
   return write_block(T_(t), coord, tsdf, weight, s2, color);
 }
 
@@ -361,6 +378,7 @@ int tsdf_table_probe_stats(tsdf_table* t, int64_t* out, double* mean_probe) {
 
 int tsdf_table_compact(tsdf_table* t) {
   NEED(t);
+  T_(t)->version++;
   return rehash_table(T_(t));
 }
 
@@ -471,6 +489,7 @@ int tsdf_integrate_depth_batch(tsdf_table* t, int32_t n_frames, const void* cons
                                double weight_cap, tsdf_integration_stats* stats,
                                int32_t* n_done) {
   NEED(t);
+  T_(t)->version++;
   if (n_frames <= 0) {
     *n_done = 0;
     return TSDF_OK;
@@ -505,6 +524,7 @@ int tsdf_integrate_depth_window(tsdf_table* t, int32_t n_frames, const void* con
                                int32_t all_levels, double fill_limit,
                                tsdf_merge_stats* merge_stats) {
   NEED(t);
+  T_(t)->version++;
   if (n_frames <= 0) {
     *n_done = 0;
     return TSDF_OK;
@@ -572,6 +592,7 @@ int tsdf_depth_window_update(tsdf_table* t, const uint64_t* received, int32_t wo
                              double sigma, double min_frac, double min_w, int32_t all_levels,
                              tsdf_integration_stats* stats, tsdf_merge_stats* merge_stats) {
   NEED(t);
+  T_(t)->version++;
   const int B = T_(t)->win.B;
   std::vector<IntegrationStats> st(std::max(B, 1));
   MergeArgs ma{sigma, min_frac, min_w, all_levels, 0.0};

@@ -66,6 +66,9 @@ struct Table {
   int lidar_mode = 0;
   // merge-pass audit: level decisions within 1e-6 relative of sigma so far
   uint64_t merge_audit = 0;
+  // bumped by every call that can change the map (tsdf_table_version): host
+  // snapshots of heap contents stay valid while it is unchanged
+  uint64_t version = 0;
   uint32_t call_id = 0;
   double depth_scale = 1.0;  // raw u16 depth units per metre (tsdf_table_set_depth_scale)
   Buf mesh_out;                   // the last extract_mesh_begin result (device)

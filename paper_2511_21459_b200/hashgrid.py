@@ -98,6 +98,16 @@ class BlockHeap:
         return self.occupied / self.capacity if self.capacity else 0.0
 
     def _snapshot(self):
+        # one export per map change (tsdf_table_version), not per attribute read
+        ver = self._table.version
+        cached = self.__dict__.get("_snap")
+        if cached is not None and cached[0] == ver:
+            return cached[1]
+        out = self._export()
+        self.__dict__["_snap"] = (ver, out)
+        return out
+
+    def _export(self):
         coords, handles, t, w, s2, c = self._table.export_level(self.level)
         n = self.capacity * self.nvox
         out = {"tsdf": np.zeros(n), "weight": np.zeros(n), "s2": np.zeros(n),
@@ -176,6 +186,13 @@ class HashTable:
         if getattr(self, "_depth_scale", 1.0) != depth_scale:
             N.check(N.lib().tsdf_table_set_depth_scale(self._h, depth_scale), "set_depth_scale")
             self._depth_scale = depth_scale
+
+    @property
+    def version(self) -> int:
+        """Bumped by every call that can change the map."""
+        out = C.c_uint64()
+        N.check(N.lib().tsdf_table_version(self._h, C.byref(out)), "version")
+        return int(out.value)
 
     @property
     def cuda_stream(self) -> int:

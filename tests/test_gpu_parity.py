@@ -699,3 +699,22 @@ def test_sharded_window_union_equals_single_gpu(world):
         assert np.array_equal(uc[order], ref[0])
         for i in (2, 3, 4, 5):
             assert np.array_equal(np.concatenate([p[i] for p in parts])[order], ref[i])
+
+
+def test_heap_snapshots_are_cached_per_map_version():
+    """heaps[l].tsdf & co. (read-only host snapshots) are exported once per
+    map change (tsdf_table_version), not on every attribute read."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    f = synth.render_frames("room", 2, 64, 48)
+    t = P.HashTable(100003, 10, 7, 0.08, (20000, 1000))
+    P.integrate_depth(t, f[0], 0.03)
+    v0 = t.version
+    a, b = t.heaps[0].tsdf, t.heaps[0].weight
+    assert t.heaps[0].tsdf is a and t.heaps[0].weight is b and t.version == v0
+    P.integrate_depth(t, f[1], 0.03)
+    assert t.version > v0
+    a2 = t.heaps[0].tsdf
+    assert a2 is not a and not np.array_equal(a2, a)
+    t.remove(tuple(t.heaps[0].coords[np.nonzero(t.heaps[0].live)[0][0]]))
+    assert t.heaps[0].occupied == int(t.heaps[0].live.sum())
