@@ -718,3 +718,45 @@ def test_heap_snapshots_are_cached_per_map_version():
     assert a2 is not a and not np.array_equal(a2, a)
     t.remove(tuple(t.heaps[0].coords[np.nonzero(t.heaps[0].live)[0][0]]))
     assert t.heaps[0].occupied == int(t.heaps[0].live.sum())
+
+
+def test_c5_two_million_point_scan_vs_oracle():
+    """BASELINE config 5's LiDAR part: one 128 x 16384-column scan (~2 M
+    returns, 100 m range, 1.6 m blocks) against the oracle -- stats and the
+    full state bit-identical in the ordered mode, and the chunked mode
+    within the north star's tolerance with exact keys and weights."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    scan = synth.lidar_frames(1, 128, 16384)[0]
+    assert len(scan.points) > 1_800_000
+    caps, nh = (600000, 20000), 8000009
+    o = PU.OracleBackend(nh, 1.6, caps)
+    so = o.points(scan, 0.8)
+    ref = o.state()
+    g = PU.GpuBackend(nh, 1.6, caps)
+    assert g.points(scan, 0.8) == so
+    assert_states_match(g.state(), ref)
+    g.close()
+    c = PU.GpuBackend(nh, 1.6, caps)
+    c.t.set_lidar_mode("chunked")
+    assert c.points(scan, 0.8) == so
+    assert_states_match(c.state(), ref, exact=False)
+    c.close()
+
+
+def test_c5_1024x768_depth_frames_vs_oracle():
+    """BASELINE config 5's depth part: the first frames of the large-room
+    sweep at 1024 x 768, 5 mm voxels, f32 depth + u8 colour, a merge pass at
+    all levels -- bit-identical to the oracle."""
+    from paper_2511_21459_b200 import synth
+    frames = synth.render_frames("large_room", 2, 1024, 768, depth_dtype=np.float32,
+                                 color_dtype=np.uint8, sweep=500)
+    caps, nh = (300000, 30000, 5000), 8000009
+    res = []
+    for b in (PU.GpuBackend(nh, 0.04, caps), PU.OracleBackend(nh, 0.04, caps)):
+        st = [b.depth(f, 0.015) for f in frames]
+        ms = b.merge(2.5e-5, all_levels=True)
+        res.append((st, ms, b.state()))
+    assert res[0][0] == res[1][0] and res[0][1] == res[1][1]
+    assert res[0][0][0]["measurements"] > 700000
+    assert_states_match(res[0][2], res[1][2])
