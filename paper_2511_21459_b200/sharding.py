@@ -376,15 +376,37 @@ def unpack_keys(keys) -> np.ndarray:
     return np.stack([(k >> np.uint64(42)) & m, (k >> np.uint64(21)) & m, k & m], axis=1).astype(np.int64) - _BIAS
 
 
-def _lookup(sorted_keys, coords):
-    """Index into sorted_keys of each coordinate row, -1 where absent."""
-    c = np.asarray(coords, dtype=np.int64)
-    if len(sorted_keys) == 0:
-        return np.full(len(c), -1, dtype=np.int64)
-    ok = np.all((c >= -_BIAS) & (c < _BIAS), axis=1)
-    k = pack_keys(np.where(ok[:, None], c, 0))
-    i = np.minimum(np.searchsorted(sorted_keys, k), len(sorted_keys) - 1)
-    return np.where(ok & (sorted_keys[i] == k), i, -1)
+class _BlockIndex:
+    """coordinate -> index into a sorted key array: a dense grid over the
+    blocks' bounding box (plus a one-block margin) when it is small enough,
+    else binary search on the packed keys."""
+
+    def __init__(self, sorted_keys):
+        self.keys = sorted_keys
+        self.grid = None
+        if len(sorted_keys):
+            c = unpack_keys(sorted_keys)
+            self.lo = c.min(axis=0) - 1
+            ext = c.max(axis=0) + 2 - self.lo
+            if int(np.prod(ext)) <= 64 << 20:
+                self.ext = ext
+                self.grid = np.full(tuple(ext.tolist()), -1, dtype=np.int64)
+                g = c - self.lo
+                self.grid[g[:, 0], g[:, 1], g[:, 2]] = np.arange(len(c))
+
+    def __call__(self, coords):
+        c = np.asarray(coords, dtype=np.int64)
+        if len(self.keys) == 0:
+            return np.full(len(c), -1, dtype=np.int64)
+        if self.grid is not None:
+            g = c - self.lo
+            ok = np.all((g >= 0) & (g < self.ext), axis=1)
+            g = np.where(ok[:, None], g, 0)
+            return np.where(ok, self.grid[g[:, 0], g[:, 1], g[:, 2]], -1)
+        ok = np.all((c >= -_BIAS) & (c < _BIAS), axis=1)
+        k = pack_keys(np.where(ok[:, None], c, 0))
+        i = np.minimum(np.searchsorted(self.keys, k), len(self.keys) - 1)
+        return np.where(ok & (self.keys[i] == k), i, -1)
 
 
 def mesh_plan(summaries, world: int, iso: float = 0.0, n_levels: int = 2) -> dict:
@@ -400,20 +422,24 @@ def mesh_plan(summaries, world: int, iso: float = 0.0, n_levels: int = 2) -> dic
     order = np.argsort(keys, kind="stable")
     keys, levels, obs, lo, hi = keys[order], levels[order], obs[order], lo[order], hi[order]
     coords = unpack_keys(keys)
+    lookup = _BlockIndex(keys)
+    # every block's 27 neighbours (indices into keys, -1 absent), once; on
+    # the dense grid (one-block margin) no bounds checks are needed
+    if lookup.grid is not None and len(keys):
+        g = coords - lookup.lo
+        nbr = np.stack([lookup.grid[g[:, 0] + d[0], g[:, 1] + d[1], g[:, 2] + d[2]] for d in _NBR])
+    else:
+        nbr = np.stack([lookup(coords + d) for d in _NBR]) if len(keys) else np.zeros((27, 0), np.int64)
     # 27-neighbourhood straddle test (meshing.py:440-456; k_keep)
-    nlo = np.full(len(keys), np.inf)
-    nhi = np.full(len(keys), -np.inf)
-    for d in _NBR:
-        j = _lookup(keys, coords + d)
-        use = (j >= 0) & obs[np.maximum(j, 0)]
-        nlo = np.where(use, np.minimum(nlo, lo[np.maximum(j, 0)]), nlo)
-        nhi = np.where(use, np.maximum(nhi, hi[np.maximum(j, 0)]), nhi)
+    use = (nbr >= 0) & obs[np.maximum(nbr, 0)]
+    nlo = np.where(use, lo[np.maximum(nbr, 0)], np.inf).min(axis=0)
+    nhi = np.where(use, hi[np.maximum(nbr, 0)], -np.inf).max(axis=0)
     kept = obs & (nlo <= iso) & (iso <= nhi)
-    per_level = [keys[kept & (levels == l)] for l in range(n_levels)]  # ascending = canonical
+    per_level = [np.nonzero(kept & (levels == l))[0] for l in range(n_levels)]  # indices, canonical
     # chunks of 256 per level, levels concatenated; contiguous runs per rank
     chunks = []  # (level, start, stop)
     for l, kl in enumerate(per_level):
-        chunks += [(l, s, min(s + 256, len(kl))) for s in range(0, len(kl), 256)]
+        chunks += [(l, s0, min(s0 + 256, len(kl))) for s0 in range(0, len(kl), 256)]
     total = sum(len(k) for k in per_level)
     bounds, acc, r = [0], 0, 1
     for ci, (l, a, b) in enumerate(chunks):
@@ -427,16 +453,11 @@ def mesh_plan(summaries, world: int, iso: float = 0.0, n_levels: int = 2) -> dic
         parts = [[] for _ in range(n_levels)]
         for l, a, b in chunks[bounds[rk]:bounds[rk + 1]]:
             parts[l].append(per_level[l][a:b])
-        ek = [np.concatenate(p) if p else np.zeros(0, np.uint64) for p in parts]
-        emit.append({"keys": np.concatenate(ek) if ek else np.zeros(0, np.uint64),
-                     "level_counts": [len(x) for x in ek]})
-        allk = emit[-1]["keys"]
-        if len(allk):
-            c = unpack_keys(allk)
-            j = np.concatenate([_lookup(keys, c + d) for d in _NBR])
-            need.append(np.unique(keys[j[j >= 0]]))
-        else:
-            need.append(np.zeros(0, np.uint64))
+        idx = [np.concatenate(p) if p else np.zeros(0, np.int64) for p in parts]
+        allidx = np.concatenate(idx)
+        emit.append({"keys": keys[allidx], "level_counts": [len(x) for x in idx]})
+        j = nbr[:, allidx].ravel()
+        need.append(keys[np.unique(j[j >= 0])])
     return {"emit": emit, "need": need, "kept": int(total), "chunks": len(chunks), "bounds": bounds}
 
 
