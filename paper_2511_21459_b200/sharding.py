@@ -671,7 +671,7 @@ def integrate_depth_window_sharded(table, frames, tau, dist, torch, group=None, 
     cap = getattr(table, "_win_cap", 8192)
     for _ in range(3):
         stride = B * (cap + 1)
-        exch = torch.empty(world * stride, dtype=torch.int64, device=dev)
+        exch = torch.zeros(world * stride, dtype=torch.int64, device=dev)
         depth_window_walk(table, caps, exch, cap)
         _torch_waits_for_table(table, torch)
         # the largest bucket of the window, over every rank (one small read)
@@ -728,7 +728,7 @@ def integrate_depth_window_local(tables, frames, tau, sigma_threshold: float = 0
     cap_all = torch.stack(caps).max(0).values.contiguous()
     cap = bucket_cap or 8192
     stride = B * (cap + 1)
-    exch = [torch.empty(world * stride, dtype=torch.int64, device=dev) for _ in range(world)]
+    exch = [torch.zeros(world * stride, dtype=torch.int64, device=dev) for _ in range(world)]
     for r, t in enumerate(tables):
         depth_window_walk(t, cap_all, exch[r], cap)
     torch.cuda.synchronize()
