@@ -50,7 +50,8 @@ def main(note, *reps):
                               "l2_hit_pct": round(m.get("l2hit", 0), 2),
                               "occupancy_pct": round(m.get("occ", 0), 2),
                               "capture": Path(rep).name}
-    out = ROOT / "profiles" / "ncu_summary.json"
+    import os
+    out = Path(os.environ.get("NCU_SUMMARY_OUT", ROOT / "profiles" / "ncu_summary.json"))
     out.write_text(json.dumps(d, indent=1, sort_keys=True) + "\n")
     print(json.dumps(d, indent=1, sort_keys=True))
 
