@@ -451,7 +451,9 @@ def run_b200(name, W, K, rank, world, dist, torch, frames=None):
     achieved = (top_bytes / top_n) / ((top_ms / top_n) * 1e-3) / 1e9 if top_ms > 0 else 0.0
     path_gbs = B["path"] / (dev_ms * 1e-3) / 1e9
     ncu, ncu_note = ncu_profile()
-    traffic = ncu.get("kernels", {}).get(top_name, {}).get("dram_bytes")
+    kt = ncu.get("kernels", {}).get(top_name, {})
+    traffic = kt.get("dram_bytes") if str(kt.get("capture", "")).startswith(
+        "room" if wl["kind"] == "depth" else "lidar") else None
     clocks = sampler.summary()
     # the binding resource of the walk is instruction issue (FP64 DDA
     # steps), not HBM: its issue roofline = the warp instructions one launch
@@ -465,6 +467,9 @@ def run_b200(name, W, K, rank, world, dist, torch, frames=None):
         steps = work["dda_steps"] / max(w_n, 1)
         ms_launch = w_ms / max(w_n, 1)
         kw = ncu.get("kernels", {}).get(walk, {})
+        # the capture must be of this workload's walk (room vs lidar launches differ)
+        if not str(kw.get("capture", "")).startswith("room" if wl["kind"] == "depth" else "lidar"):
+            kw = {}
         secondary = {"bound": "issue (FP64 DDA steps)", "kernel": walk,
                      "dda_steps_per_launch": round(steps), "ms_per_launch": round(ms_launch, 4),
                      "gsteps_per_s": round(steps / (ms_launch * 1e-3) / 1e9, 3)}
