@@ -276,7 +276,7 @@ __device__ void gather_corner(const DevTable& t, const NbInfo* nb, const int64_t
 }
 
 template <bool kWrite>
-__global__ void __launch_bounds__(kMcThreads) k_mc(McArgs A) {
+__global__ void __launch_bounds__(kMcThreads, 2) k_mc(McArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   McSmem& S = *reinterpret_cast<McSmem*>(smem_raw);
   typedef cub::BlockScan<int32_t, kMcThreads> Scan;
