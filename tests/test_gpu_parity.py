@@ -760,3 +760,27 @@ def test_c5_1024x768_depth_frames_vs_oracle():
     assert res[0][0] == res[1][0] and res[0][1] == res[1][1]
     assert res[0][0][0]["measurements"] > 700000
     assert_states_match(res[0][2], res[1][2])
+
+
+def test_walk_cluster_dsmem_filter_matches_oracle():
+    """The depth walk launched as 4-CTA thread-block clusters
+    (TSDF_WALK_CLUSTER=4): the cluster-wide first-sighting filter in
+    distributed shared memory leaves the allocation bit-identical (a fresh
+    process, since the launch shape is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import numpy as np, parity_utils as PU\n"
+        "spec = dict(scene='large_room', frames=3, width=160, height=120, edge=0.04, tau=0.015,\n"
+        "            caps=(60000, 10000, 4000), n_hash=1000003, sigma=2.5e-5, cadence=3, all_levels=True,\n"
+        "            depth_dtype=np.float32, color_dtype=np.uint8)\n"
+        "g, sg, mg, _ = PU.run_depth_scenario('gpu', **spec)\n"
+        "o, so, mo, _ = PU.run_depth_scenario('oracle', **spec)\n"
+        "assert sg == so and mg == mo\n"
+        "assert PU.state_digest(g.state()) == PU.state_digest(o.state())\n"
+        "print('ok', sg[0]['blocks_allocated'])\n") % (str(PU.ROOT), str(PU.ROOT / "tests"))
+    env = dict(os.environ, TSDF_WALK_CLUSTER="4")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
