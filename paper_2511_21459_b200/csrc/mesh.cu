@@ -781,14 +781,64 @@ struct DevMesh {
 };
 
 // D2H of a device mesh into caller-owned host arrays
+// The mesh is one contiguous device range (v, n, c, tri).  Copies to
+// pageable host memory run at a few GB/s, so large meshes go through two
+// pinned 4 MB staging buffers: the D2H of chunk k overlaps the host copy of
+// chunk k-1 out of the other buffer into the caller's arrays.
 static int mesh_to_host(const DevMesh& m, cudaStream_t st, double* v, double* n, double* c, int64_t* tri) {
-  if (m.nv) {
-    MCK(cudaMemcpyAsync(v, m.v(), m.nv * 24, cudaMemcpyDeviceToHost, st));
-    MCK(cudaMemcpyAsync(n, m.n(), m.nv * 24, cudaMemcpyDeviceToHost, st));
-    MCK(cudaMemcpyAsync(c, m.c(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+  const size_t segs[4] = {(size_t)m.nv * 24, (size_t)m.nv * 24, (size_t)m.nv * 24, (size_t)m.nt * 24};
+  char* dst[4] = {(char*)v, (char*)n, (char*)c, (char*)tri};
+  const size_t total = segs[0] + segs[1] + segs[2] + segs[3];
+  constexpr size_t kChunk = 4u << 20;
+  // per host thread (tables on different threads extract concurrently)
+  static thread_local char* pin[2] = {nullptr, nullptr};
+  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (total >= 2 * kChunk && !pin[0]) {
+    if (cudaMallocHost(&pin[0], kChunk) != cudaSuccess || cudaMallocHost(&pin[1], kChunk) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      pin[0] = pin[1] = nullptr;
+    }
   }
-  if (m.nt) MCK(cudaMemcpyAsync(tri, m.tri(), m.nt * 24, cudaMemcpyDeviceToHost, st));
-  MCK(cudaStreamSynchronize(st));
+  if (total < 2 * kChunk || !pin[0]) {
+    if (m.nv) {
+      MCK(cudaMemcpyAsync(v, m.v(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+      MCK(cudaMemcpyAsync(n, m.n(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+      MCK(cudaMemcpyAsync(c, m.c(), m.nv * 24, cudaMemcpyDeviceToHost, st));
+    }
+    if (m.nt) MCK(cudaMemcpyAsync(tri, m.tri(), m.nt * 24, cudaMemcpyDeviceToHost, st));
+    MCK(cudaStreamSynchronize(st));
+    return kOk;
+  }
+  const char* src = (const char*)m.v();
+  // host copy of device bytes [off, off + len) out of a staging buffer
+  auto scatter = [&](const char* buf, size_t off, size_t len) {
+    size_t seg_off = 0;
+    for (int i = 0; i < 4 && len; i++) {
+      if (off < seg_off + segs[i]) {
+        const size_t in = off - seg_off, take = std::min(len, segs[i] - in);
+        memcpy(dst[i] + in, buf, take);
+        buf += take;
+        off += take;
+        len -= take;
+      }
+      seg_off += segs[i];
+    }
+  };
+  const size_t nchunks = (total + kChunk - 1) / kChunk;
+  for (size_t k = 0; k <= nchunks; k++) {
+    if (k < nchunks) {
+      const size_t off = k * kChunk, len = std::min(kChunk, total - off);
+      MCK(cudaMemcpyAsync(pin[k & 1], src + off, len, cudaMemcpyDeviceToHost, st));
+      MCK(cudaEventRecord(ev[k & 1], st));
+    }
+    if (k > 0) {
+      const size_t j = k - 1, off = j * kChunk, len = std::min(kChunk, total - off);
+      MCK(cudaEventSynchronize(ev[j & 1]));
+      scatter(pin[j & 1], off, len);
+    }
+  }
   return kOk;
 }
 
