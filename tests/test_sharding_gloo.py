@@ -311,3 +311,23 @@ def test_mesh_plan_partitions_the_kept_list():
                 k = int(pack_keys((c + np.array(d) - 1)[None])[0])
                 if k in live:
                     assert k in nd
+
+
+def test_mesh_plan_empty_and_sparse_maps():
+    """mesh_plan on an empty map and on a map whose bounding box is too large
+    for the dense index grid (binary-search fallback): same plan shape."""
+    import numpy as np
+    from paper_2511_21459_b200.sharding import mesh_plan, pack_keys
+    empty = {"keys": np.zeros(0, np.uint64), "levels": np.zeros(0, np.int32), "obs": np.zeros(0, np.uint8),
+             "lo": np.zeros(0), "hi": np.zeros(0)}
+    p = mesh_plan([empty, empty], 3, 0.0, 2)
+    assert p["kept"] == 0 and all(len(e["keys"]) == 0 for e in p["emit"]) and all(len(n) == 0 for n in p["need"])
+    # two clusters of blocks ~1e6 blocks apart: the grid would be too large
+    c = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [900000, 5, 5], [900001, 5, 5]], dtype=np.int64)
+    s = {"keys": pack_keys(c), "levels": np.zeros(5, np.int32), "obs": np.ones(5, np.uint8),
+         "lo": np.full(5, -0.01), "hi": np.full(5, 0.01)}
+    p = mesh_plan([s], 2, 0.0, 2)
+    assert p["kept"] == 5
+    got = set(np.concatenate([e["keys"] for e in p["emit"]]).tolist())
+    assert got == set(pack_keys(c).tolist())
+    assert set(np.concatenate(p["need"]).tolist()) == got
