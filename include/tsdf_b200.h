@@ -389,6 +389,12 @@ int64_t tsdf_table_slots(tsdf_table *t);
  * live key (1 = at its home slot), [3] rebuilds so far; *mean_probe = the
  * average probe length of the live keys. */
 int tsdf_table_probe_stats(tsdf_table *t, int64_t *out, double *mean_probe);
+
+/* Replaces HashTable.probe_length (hashgrid.py:194-212), batched: out[j] =
+ * index slots examined for coords[j] (host int64 [n][3]) until it resolves,
+ * 1 = at its home slot; for an absent key, until the empty slot that proves
+ * it absent.  Diagnostics only; the table is unchanged. */
+int tsdf_probe_length(tsdf_table *t, const int64_t *coords, int64_t n, int32_t *out);
 int tsdf_table_compact(tsdf_table *t);
 int tsdf_device_info(int32_t *sm_major, int32_t *sm_minor, int32_t *num_sms);
 

@@ -144,6 +144,7 @@ def lib():
     L.tsdf_table_slots.argtypes = [_ptr]
     L.tsdf_device_info.argtypes = [C.POINTER(i32)] * 3
     L.tsdf_table_probe_stats.argtypes = [_ptr, _i64p, C.POINTER(dbl)]
+    L.tsdf_probe_length.argtypes = [_ptr, _i64p, C.c_int64, C.c_void_p]
     L.tsdf_table_compact.argtypes = [_ptr]
     L.tsdf_dda_blocks.argtypes = [_ptr, _ptr, i64, dbl, i32, C.POINTER(C.POINTER(i64)),
                                   C.POINTER(C.POINTER(i64)), C.POINTER(i64)]

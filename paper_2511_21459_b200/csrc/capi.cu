@@ -376,6 +376,11 @@ int tsdf_table_probe_stats(tsdf_table* t, int64_t* out, double* mean_probe) {
   return TSDF_OK;
 }
 
+int tsdf_probe_length(tsdf_table* t, const int64_t* coords, int64_t n, int32_t* out) {
+  NEED(t);
+  return probe_length(T_(t), coords, n, out);
+}
+
 int tsdf_table_compact(tsdf_table* t) {
   NEED(t);
   T_(t)->version++;

@@ -158,6 +158,7 @@ struct ProbeStats {
   double mean_probe;
 };
 int probe_stats(Table* T, ProbeStats* out);
+int probe_length(Table* T, const int64_t* coords, int64_t n, int32_t* out);
 
 struct DepthArgs {
   const void* depth;

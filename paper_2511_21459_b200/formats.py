@@ -207,9 +207,24 @@ def write_mesh(mesh, path) -> None:
         raise FormatError(f"cannot write mesh to {path}: {exc}") from exc
 
 
+def _vertex_layout(props: list) -> np.dtype:
+    """Vertex record of the PLYs this package writes: xyz, then optional
+    normals, rgb and scale, in that order (formats.py:64-116)."""
+    names = {p.split()[-1] for p in props}
+    fields = [("xyz", "<f4", (3,))]
+    if "nx" in names:
+        fields.append(("n", "<f4", (3,)))
+    if "red" in names:
+        fields.append(("rgb", "u1", (3,)))
+    if "scale" in names:
+        fields.append(("scale", "<f4"))
+    return np.dtype(fields)
+
+
 def read_mesh(path):
-    """PLY written by write_mesh -> Mesh (f64 positions / normals, colours
-    in [0, 1])."""
+    """A binary little-endian PLY written by write_mesh / write_point_cloud /
+    write_seeds -> Mesh (f64 positions; normals 0 and colours 0.5 when the
+    file has none; no faces for a point cloud)."""
     from .meshing import Mesh
     try:
         blob = Path(path).read_bytes()
@@ -221,14 +236,72 @@ def read_mesh(path):
     lines = blob[:end].decode("ascii", errors="replace").splitlines()
     if "format binary_little_endian 1.0" not in lines:
         raise FormatError(f"{path}: only binary little-endian PLY is supported")
-    counts = {p[1]: int(p[2]) for p in (l.split() for l in lines) if len(p) == 3 and p[0] == "element"}
+    counts, props, elem = {}, {}, None
+    for line in lines:
+        parts = line.split()
+        if parts[:1] == ["element"]:
+            elem = parts[1]
+            counts[elem], props[elem] = int(parts[2]), []
+        elif parts[:1] == ["property"] and elem is not None:
+            props[elem].append(line)
     body = blob[end + len(b"end_header\n"):]
+    vdt = _vertex_layout(props.get("vertex", []))
     nv, nt = counts.get("vertex", 0), counts.get("face", 0)
-    if len(body) < nv * _PLY_VERTEX.itemsize + nt * _PLY_FACE.itemsize:
+    if len(body) < nv * vdt.itemsize + nt * _PLY_FACE.itemsize:
         raise FormatError(f"{path}: truncated PLY body")
-    v = np.frombuffer(body, dtype=_PLY_VERTEX, count=nv)
-    f = np.frombuffer(body, dtype=_PLY_FACE, count=nt, offset=nv * _PLY_VERTEX.itemsize)
-    if nt and not (f["k"] == 3).all():
-        raise FormatError(f"{path}: only triangle faces are supported")
-    return Mesh(vertices=v["xyz"].astype(np.float64), normals=v["n"].astype(np.float64),
-                colors=v["rgb"].astype(np.float64) / 255.0, triangles=f["idx"].astype(np.int64))
+    v = np.frombuffer(body, dtype=vdt, count=nv)
+    tris = np.zeros((0, 3), dtype=np.int64)
+    if nt:
+        f = np.frombuffer(body, dtype=_PLY_FACE, count=nt, offset=nv * vdt.itemsize)
+        if not (f["k"] == 3).all():
+            raise FormatError(f"{path}: only triangle faces are supported")
+        tris = f["idx"].astype(np.int64)
+    names = vdt.names
+    normals = v["n"].astype(np.float64) if "n" in names else np.zeros((nv, 3))
+    colors = v["rgb"].astype(np.float64) / 255.0 if "rgb" in names else np.full((nv, 3), 0.5)
+    return Mesh(vertices=v["xyz"].astype(np.float64), normals=normals, colors=colors,
+                triangles=tris)
+
+
+# -- point clouds and splat seeds (binary little-endian PLY, formats.py:119-180)
+
+def _u8_color(c) -> np.ndarray:
+    return np.clip(np.round(np.asarray(c) * 255.0), 0, 255).astype(np.uint8)
+
+
+def _write_vertex_ply(path, props: str, rec: np.ndarray) -> None:
+    head = ("ply\nformat binary_little_endian 1.0\n"
+            f"element vertex {len(rec)}\n{props}end_header\n")
+    with open(Path(path), "wb") as fh:
+        fh.write(head.encode("ascii"))
+        fh.write(rec.tobytes())
+
+
+_XYZ_PROPS = "property float x\nproperty float y\nproperty float z\n"
+_RGB_PROPS = "property uchar red\nproperty uchar green\nproperty uchar blue\n"
+
+
+def write_point_cloud(points, path, colors=None) -> None:
+    """Points (and optional colours in [0, 1]) -> PLY vertices: f32 xyz,
+    u8 rgb (round(c * 255) clipped)."""
+    xyz = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    layout = [("xyz", "<f4", (3,))] + ([("rgb", "u1", (3,))] if colors is not None else [])
+    rec = np.zeros(len(xyz), dtype=np.dtype(layout))
+    rec["xyz"] = xyz.astype(np.float32)
+    if colors is not None:
+        rec["rgb"] = _u8_color(colors)
+    _write_vertex_ply(path, _XYZ_PROPS + (_RGB_PROPS if colors is not None else ""), rec)
+
+
+def write_seeds(seeds, path) -> None:
+    """Splat seeds (position, colour, scale) -> PLY vertices with a float
+    `scale` property after the colour."""
+    seeds = list(seeds)
+    rec = np.zeros(len(seeds), dtype=np.dtype([("xyz", "<f4", (3,)), ("rgb", "u1", (3,)),
+                                               ("scale", "<f4")]))
+    if seeds:
+        rec["xyz"] = np.array([s.position for s in seeds], dtype=np.float64)
+        rec["rgb"] = np.clip(np.round(np.array([np.asarray(s.color, dtype=np.float64)
+                                                for s in seeds]) * 255.0), 0, 255)
+        rec["scale"] = np.array([s.scale for s in seeds], dtype=np.float64)
+    _write_vertex_ply(path, _XYZ_PROPS + _RGB_PROPS + "property float scale\n", rec)

@@ -79,7 +79,8 @@ class BlockPayload:
 
 
 class BlockHeap:
-    """Per-level view: sizes, occupancy and read-only snapshots by handle."""
+    """Per-level view: sizes, occupancy and the level's voxel arrays by
+    handle (snapshots of the device heap; item assignment writes through)."""
 
     def __init__(self, table: "HashTable", level: int, capacity: int):
         self._table = table
@@ -127,9 +128,93 @@ class BlockHeap:
         return out
 
     def __getattr__(self, name):
-        if name in ("tsdf", "weight", "s2", "color", "coords", "live"):
+        if name in _VOXEL_FIELDS:
+            return HeapField._over(self, name, self._snapshot())
+        if name in ("coords", "live"):
             return self._snapshot()[name]
         raise AttributeError(name)
+
+    def payload(self, handle: int) -> BlockPayload:
+        """Copy of the block stored at `handle` (hashgrid.py:115-125).  A
+        live block is read from the device; a free handle reads as the
+        zeros the slab holds."""
+        snap = self._snapshot()
+        h = int(handle)
+        if snap["live"][h]:
+            coord = tuple(int(v) for v in snap["coords"][h])
+            return self._table.payload(coord)
+        lo, hi = h * self.nvox, (h + 1) * self.nvox
+        return BlockPayload(coord=tuple(int(v) for v in snap["coords"][h]), level=self.level,
+                            tsdf=snap["tsdf"][lo:hi].copy(), weight=snap["weight"][lo:hi].copy(),
+                            s2=snap["s2"][lo:hi].copy(), color=snap["color"][lo:hi].copy())
+
+    def write_payload(self, handle: int, payload: BlockPayload) -> None:
+        """Overwrite the voxels of the live block at `handle`
+        (hashgrid.py:127-133); its key and level stay."""
+        snap = self._snapshot()
+        h = int(handle)
+        if not snap["live"][h]:
+            raise ValueError(f"heap slot {h} of level {self.level} holds no live block")
+        coord = tuple(int(v) for v in snap["coords"][h])
+        self._table.write_payload(coord, payload)
+
+    def _write_back(self, snap: dict, name: str, before: np.ndarray) -> None:
+        """Push the blocks whose `name` values changed in `snap` to the
+        device.  The other fields of each block are read back from the device
+        first, so a stale snapshot never overwrites them."""
+        after = snap[name]
+        diff = (before != after) & ~(np.isnan(before) & np.isnan(after))
+        rows = np.nonzero(diff.any(axis=1) if diff.ndim == 2 else diff)[0]
+        handles = np.unique(rows // self.nvox)
+        dead = [int(h) for h in handles if not snap["live"][h]]
+        if dead:
+            after[...] = before
+            raise ValueError(f"heap slot(s) {dead[:8]} of level {self.level} hold no live block; "
+                             "only live blocks can be written")
+        for h in handles:
+            coord = tuple(int(v) for v in snap["coords"][h])
+            pay = self._table.payload(coord)
+            setattr(pay, name, np.array(after[h * self.nvox:(h + 1) * self.nvox]))
+            self._table.write_payload(coord, pay)
+
+
+_VOXEL_FIELDS = ("tsdf", "weight", "s2", "color")
+
+
+class HeapField(np.ndarray):
+    """A level's flat voxel array in the reference's heap layout
+    (hashgrid.py:95-140: handle * nvox + voxel index).  Reading it is a
+    snapshot of the device heap; item assignment on the array itself writes
+    the changed blocks through to the device, which is what the reference's
+    own tests do to craft fields (tests/test_meshing.py:22-39).  Views derived
+    from it are read-only; copies are ordinary arrays."""
+
+    _owner = None
+
+    def __array_finalize__(self, obj):
+        self._owner = None          # slices / views of a field do not write through
+
+    @classmethod
+    def _over(cls, heap: "BlockHeap", name: str, snap: dict) -> "HeapField":
+        out = snap[name].view(cls)
+        out._owner = (heap, name, snap)
+        return out
+
+    def __setitem__(self, index, value):
+        if self._owner is None:
+            # a copy writes normally; a view of the snapshot is read-only and
+            # numpy says so
+            np.ndarray.__setitem__(self, index, value)
+            return
+        heap, name, snap = self._owner
+        base = snap[name]
+        before = base.copy()
+        base.setflags(write=True)
+        try:
+            np.ndarray.__setitem__(base, index, value)
+        finally:
+            base.setflags(write=False)
+        heap._write_back(snap, name, before)
 
 
 class HashTable:
@@ -318,6 +403,19 @@ class HashTable:
         col = np.ascontiguousarray(payload.color, dtype=np.float32)
         N.check(N.lib().tsdf_write_block(self._h, c, t.ctypes.data, w.ctypes.data,
                                          s2.ctypes.data, col.ctypes.data), "write_payload")
+
+    def probe_length(self, coord) -> int:
+        """Index slots examined before a find of `coord` resolves (1 = at its
+        home slot; diagnostics, hashgrid.py:194-212 -- there the count is of
+        bucket and chain entries)."""
+        return int(self.probe_lengths([coord])[0])
+
+    def probe_lengths(self, coords) -> np.ndarray:
+        c = np.ascontiguousarray(np.asarray(coords, dtype=np.int64).reshape(-1, 3))
+        out = np.zeros(len(c), dtype=np.int32)
+        if len(c):
+            N.check(N.lib().tsdf_probe_length(self._h, c, len(c), out.ctypes.data), "probe_length")
+        return out
 
     # -- batch operations ------------------------------------------------------
     def find_batch(self, coords):

@@ -158,6 +158,102 @@ def render_frames(scene_name: str, frames: int, width: int, height: int,
     return out
 
 
+scene_trajectory = trajectory   # the reference's name (synth.py:75)
+
+
+def sphere_reference(n: int = 200_000, radius: float = 1.0) -> np.ndarray:
+    """Ground-truth samples of the unit-sphere scene (synth.py:178-179)."""
+    return fibonacci_directions(n) * radius
+
+
+def frames_reference(frames: list, stride: int = 4, max_points: int = 300_000,
+                     seed: int = 0) -> np.ndarray:
+    """Observed-surface reference: every `stride`-th valid pixel of each frame
+    back-projected to world (synth.py:182-197), subsampled without
+    replacement to `max_points` with the seeded generator."""
+    parts = []
+    for f in frames:
+        rows, cols = np.nonzero(f.valid_mask())
+        rows, cols = rows[::stride], cols[::stride]
+        z = f.metres()[rows, cols]
+        k = f.intrinsics
+        cam = np.stack([(cols - k.cx) / k.fx * z, (rows - k.cy) / k.fy * z, z], axis=1)
+        parts.append(f.pose.to_world(cam))
+    pts = np.concatenate(parts)
+    if len(pts) > max_points:
+        pts = pts[np.random.default_rng(seed).choice(len(pts), size=max_points, replace=False)]
+    return pts
+
+
+def rotation_to_quaternion(rot) -> tuple:
+    """Scalar-last unit quaternion (qx, qy, qz, qw) of a proper rotation, from
+    the largest of the four |q| components (numerically safe everywhere)."""
+    m = np.asarray(rot, dtype=np.float64)
+    tr = m[0, 0] + m[1, 1] + m[2, 2]
+    cand = np.array([1.0 + m[0, 0] - m[1, 1] - m[2, 2], 1.0 - m[0, 0] + m[1, 1] - m[2, 2],
+                     1.0 - m[0, 0] - m[1, 1] + m[2, 2], 1.0 + tr])
+    big = int(np.argmax(cand))
+    r = 0.5 * np.sqrt(cand[big])
+    s = 0.25 / r
+    sym = {(0, 1): m[0, 1] + m[1, 0], (0, 2): m[0, 2] + m[2, 0], (1, 2): m[1, 2] + m[2, 1]}
+    skew = (m[2, 1] - m[1, 2], m[0, 2] - m[2, 0], m[1, 0] - m[0, 1])
+    q = np.zeros(4)
+    q[big] = r
+    for j in range(3):
+        if j != big:
+            q[j] = (skew[j] if big == 3 else sym[tuple(sorted((big, j)))]) * s
+    if big != 3:
+        q[3] = skew[big] * s
+    q /= np.linalg.norm(q)
+    return tuple(float(x) for x in q)
+
+
+def generate_dataset(scene_name: str, out_dir, frames: int = 30, width: int = 96, height: int = 72,
+                     sensor_mode: str = "depth", depth_scale: float = 5000.0,
+                     cloud_stride: int = 2):
+    """Write a fixture dataset in the reference's layout (synth.py:230-274):
+    intrinsics.txt, trajectory.txt (t = 0.1 i), depth/ + rgb/ 16-bit and RGB
+    PNGs (raw = round(z * depth_scale)) or clouds/*.pcb (every
+    `cloud_stride`-th valid pixel, sensor frame, with colour), and a
+    reference.ply ground-truth point cloud.  Returns the directory."""
+    from pathlib import Path
+
+    from PIL import Image
+
+    from .datasets import write_pointcloud_file
+    from .formats import write_point_cloud
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    scene = make_scene(scene_name)
+    intr = default_intrinsics(scene_name, width, height)
+    (out / "intrinsics.txt").write_text(f"{intr.fx} {intr.fy} {intr.cx} {intr.cy}\n")
+    lines, rendered = [], []
+    for i, pose in enumerate(trajectory(scene, frames)):
+        qx, qy, qz, qw = rotation_to_quaternion(pose.rotation)
+        tx, ty, tz = pose.translation
+        lines.append(f"{0.1 * i:.6f} {tx:.9f} {ty:.9f} {tz:.9f} {qx:.9f} {qy:.9f} {qz:.9f} {qw:.9f}")
+        depth, rgb = render_depth(scene, pose, intr, width, height)
+        frame = DepthFrame(depth=depth, intrinsics=intr, pose=pose, color=rgb)
+        rendered.append(frame)
+        if sensor_mode == "depth":
+            for sub in ("depth", "rgb"):
+                (out / sub).mkdir(exist_ok=True)
+            raw = np.clip(np.round(depth * depth_scale), 0, 65535).astype(np.uint16)
+            Image.fromarray(raw).save(out / "depth" / f"{i:06d}.png")
+            Image.fromarray((rgb * 255).astype(np.uint8)).save(out / "rgb" / f"{i:06d}.png")
+        else:
+            (out / "clouds").mkdir(exist_ok=True)
+            rows, cols = np.nonzero(frame.valid_mask())
+            rows, cols = rows[::cloud_stride], cols[::cloud_stride]
+            z = depth[rows, cols]
+            pts = np.stack([(cols - intr.cx) / intr.fx * z, (rows - intr.cy) / intr.fy * z, z], axis=1)
+            write_pointcloud_file(out / "clouds" / f"{i:06d}.pcb", pts, rgb[rows, cols])
+    (out / "trajectory.txt").write_text("\n".join(lines) + "\n")
+    truth = sphere_reference(150_000) if scene_name == "sphere" else frames_reference(rendered)
+    write_point_cloud(truth, out / "reference.ply")
+    return out
+
+
 # ---------------------------------------------------------------------------
 # 128-beam spinning LiDAR (SURVEY §8d, config 3)
 # ---------------------------------------------------------------------------

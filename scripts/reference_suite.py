@@ -1,0 +1,107 @@
+"""Run the reference's OWN test suite against this package (host-mirror mode).
+
+The reference's tests (`/root/reference/pkg/tests`) import `tsdfusion.*`.
+This harness registers this package under that name -- every submodule the
+tests import maps to ours -- and runs them unmodified with pytest on a GPU
+box, so they exercise the CUDA path through the same Python API a user of
+the reference calls.  It is a second, independent parity harness beside
+tests/ (which compares against the oracle and reference-generated goldens).
+
+  python scripts/reference_suite.py stage   # here: copy the suite into oracle/_ref/
+  python scripts/reference_suite.py run     # GPU box: run it, summary -> gpurun_out/
+
+The staged copy lives under oracle/_ref/ (git-ignored, like the compiled
+reference: it travels to the GPU box with the snapshot but never enters the
+repository history).  Modules the tier leaves out of scope (the CLI and the
+reference's own benchmark/report driver) are not aliased, so the
+two test files importing them report as collection errors; everything else
+runs.
+"""
+from __future__ import annotations
+
+import importlib
+import json
+import shutil
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+STAGE = ROOT / "oracle" / "_ref" / "reference_tests"
+REF_TESTS = Path("/root/reference/pkg/tests")
+
+# tsdfusion submodule -> ours (names the reference's tests import)
+ALIASES = {
+    "adapt": "adapt", "config": "config", "datasets": "datasets", "dda": "dda",
+    "errors": "errors", "formats": "formats", "geometry": "geometry", "hashgrid": "hashgrid",
+    "integrate": "integrate", "meshing": "meshing", "metrics": "metrics", "pipeline": "pipeline",
+    "quadtree": "quadtree", "streaming": "streaming", "synth": "synth", "mc_tables": "_mc_tables",
+}
+OUT_OF_SCOPE = ("cli", "bench", "report")
+
+
+def stage() -> None:
+    if not REF_TESTS.is_dir():
+        sys.exit(f"{REF_TESTS} not found (stage in the build container)")
+    if STAGE.exists():
+        shutil.rmtree(STAGE)
+    STAGE.mkdir(parents=True)
+    for f in sorted(REF_TESTS.glob("*.py")):
+        shutil.copy2(f, STAGE / f.name)
+    print(f"staged {len(list(STAGE.glob('test_*.py')))} test files into {STAGE}")
+
+
+def alias() -> None:
+    sys.path.insert(0, str(ROOT))
+    pkg = importlib.import_module("paper_2511_21459_b200")
+    sys.modules["tsdfusion"] = pkg
+    for ref_name, ours in ALIASES.items():
+        mod = importlib.import_module(f"paper_2511_21459_b200.{ours}")
+        sys.modules[f"tsdfusion.{ref_name}"] = mod
+        setattr(pkg, ref_name, mod)
+
+
+def run() -> int:
+    import pytest
+
+    if not STAGE.is_dir():
+        sys.exit(f"{STAGE} missing: run `python scripts/reference_suite.py stage` in the build container")
+    alias()
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    xml = out / "reference_suite.xml"
+    t0 = time.time()
+    rc = pytest.main([str(STAGE), "-q", "-p", "no:cacheprovider", "--rootdir", str(STAGE),
+                      "--continue-on-collection-errors",
+                      f"--junitxml={xml}", "-o", "addopts=", "-o", "markers=slow"])
+    summary = summarize(xml)
+    summary["wall_s"] = round(time.time() - t0, 1)
+    (out / "reference_suite.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps({k: v for k, v in summary.items() if k != "cases"}, indent=1))
+    return int(rc)
+
+
+def summarize(xml: Path) -> dict:
+    import xml.etree.ElementTree as ET
+
+    cases, counts = [], {"passed": 0, "failed": 0, "error": 0, "skipped": 0}
+    for tc in ET.parse(xml).getroot().iter("testcase"):
+        status, msg = "passed", ""
+        for tag in ("failure", "error", "skipped"):
+            node = tc.find(tag)
+            if node is not None:
+                status = {"failure": "failed"}.get(tag, tag)
+                msg = (node.get("message") or "").splitlines()[0][:300] if node.get("message") else ""
+                break
+        counts[status] += 1
+        cases.append({"file": tc.get("classname", ""), "name": tc.get("name"), "status": status,
+                      "message": msg})
+    return {"counts": counts, "cases": cases}
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1] if len(sys.argv) > 1 else "run"
+    if mode == "stage":
+        stage()
+    else:
+        sys.exit(run())

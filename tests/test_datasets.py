@@ -23,7 +23,7 @@ def test_depth_sequence_keeps_raw_units(tmp_path):
     from paper_2511_21459_b200.datasets import read_depth_sequence
     root = write_depth_dataset(tmp_path / "d", n_frames=3)
     frames = list(read_depth_sequence(root, root / "trajectory.txt", root / "intrinsics.txt",
-                                      depth_scale=SCALE))
+                                      depth_scale=SCALE, keep_types=True))
     assert len(frames) == 3
     for f in frames:
         assert f.depth.dtype == np.uint16 and f.depth_scale == SCALE and f.raw_depth
@@ -38,9 +38,13 @@ def test_depth_sequence_matches_reference_reader(tmp_path):
     from paper_2511_21459_b200.datasets import read_depth_sequence
     root = write_depth_dataset(tmp_path / "d", n_frames=4)
     args = (root, root / "trajectory.txt", root / "intrinsics.txt")
-    mine = list(read_depth_sequence(*args, depth_scale=SCALE, workers=2))
+    mine = list(read_depth_sequence(*args, depth_scale=SCALE, workers=2, keep_types=True))
     ref = list(datasets.read_depth_sequence(*args, depth_scale=SCALE))
-    assert len(mine) == len(ref)
+    plain = list(read_depth_sequence(*args, depth_scale=SCALE, workers=2))
+    assert len(mine) == len(ref) == len(plain)
+    for a, b in zip(plain, ref):  # default: the reference's own frame types and values
+        assert a.depth.dtype == np.float64 and np.array_equal(a.depth, b.depth)
+        assert np.array_equal(a.color, b.color)
     for a, b in zip(mine, ref):
         assert np.array_equal(a.metres(), b.depth)
         assert np.array_equal(a.color.astype(np.float64) / 255.0, b.color)
@@ -55,8 +59,14 @@ def test_cloud_sequence_matches_reference_reader(tmp_path):
     datasets = _ref_datasets()
     from paper_2511_21459_b200.datasets import read_pointcloud_sequence
     root = write_cloud_dataset(tmp_path / "c")
-    mine = list(read_pointcloud_sequence(root, root / "trajectory.txt"))
+    mine = list(read_pointcloud_sequence(root, root / "trajectory.txt", keep_types=True))
     ref = list(datasets.read_pointcloud_sequence(root, root / "trajectory.txt"))
+    plain = list(read_pointcloud_sequence(root, root / "trajectory.txt"))
+    for a, b in zip(plain, ref):
+        assert np.array_equal(a.points, b.points) and a.points.dtype == np.float64
+        assert (a.colors is None) == (b.colors is None)
+        if b.colors is not None:
+            assert np.array_equal(a.colors, b.colors)
     assert len(mine) == len(ref) == 2
     for a, b in zip(mine, ref):
         assert np.array_equal(np.asarray(a.points, dtype=np.float64), b.points)

@@ -83,7 +83,7 @@ def test_depth_dataset_engine_vs_oracle(tmp_path):
                            merge_cadence=5, depth_scale=SCALE)
     eng = P.FusionEngine(cfg)
     n = 0
-    for f in read_depth_sequence(*args, depth_scale=cfg.depth_scale):
+    for f in read_depth_sequence(*args, depth_scale=cfg.depth_scale, keep_types=True):
         eng.integrate_frame(f)
         eng.maybe_merge()
         n += 1
@@ -108,7 +108,7 @@ def test_cloud_dataset_vs_oracle(tmp_path):
     root = write_cloud_dataset(tmp_path / "c", n_scans=2, beams=32, columns=256)
     t = P.HashTable(1000003, 10, 7, 1.6, (300000, 20000))
     o = PU.OracleBackend(1000003, 1.6, (300000, 20000))
-    for f in read_pointcloud_sequence(root, root / "trajectory.txt"):
+    for f in read_pointcloud_sequence(root, root / "trajectory.txt", keep_types=True):
         s = P.integrate_pointcloud(t, f, 0.8)
         assert {k: getattr(s, k) for k in PU.STAT_KEYS} == o.points(f, 0.8)
     assert PU.state_digest(_gpu_state(t)) == PU.state_digest(o.state())

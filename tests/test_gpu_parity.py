@@ -711,13 +711,49 @@ def test_heap_snapshots_are_cached_per_map_version():
     P.integrate_depth(t, f[0], 0.03)
     v0 = t.version
     a, b = t.heaps[0].tsdf, t.heaps[0].weight
-    assert t.heaps[0].tsdf is a and t.heaps[0].weight is b and t.version == v0
+    # the same export each time (fresh write-through views over one buffer)
+    assert np.shares_memory(t.heaps[0].tsdf, a) and np.shares_memory(t.heaps[0].weight, b)
+    assert t.version == v0
     P.integrate_depth(t, f[1], 0.03)
     assert t.version > v0
     a2 = t.heaps[0].tsdf
-    assert a2 is not a and not np.array_equal(a2, a)
+    assert not np.shares_memory(a2, a) and not np.array_equal(a2, a)
     t.remove(tuple(t.heaps[0].coords[np.nonzero(t.heaps[0].live)[0][0]]))
     assert t.heaps[0].occupied == int(t.heaps[0].live.sum())
+
+
+def test_heap_voxel_arrays_write_through_like_the_reference():
+    """heaps[l].tsdf[a:b] = x (how the reference's own tests craft fields,
+    tests/test_meshing.py:22-39) writes the touched live blocks to the
+    device; the other fields of those blocks are untouched; writing a slot
+    that holds no live block is refused; derived views are read-only."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200 import synth
+    f = synth.render_frames("room", 1, 64, 48)[0]
+    t = P.HashTable(100003, 10, 7, 0.08, (20000, 1000))
+    P.integrate_depth(t, f, 0.03)
+    heap = t.heaps[0]
+    h = int(np.nonzero(heap.live)[0][3])
+    coord = tuple(int(v) for v in heap.coords[h])
+    before = t.payload(coord)
+    lo, n = h * heap.nvox, heap.nvox
+    vals = np.linspace(-0.02, 0.02, n)
+    heap.tsdf[lo:lo + n] = vals
+    after = t.payload(coord)
+    assert np.array_equal(after.tsdf, vals)
+    assert np.array_equal(after.weight, before.weight) and np.array_equal(after.s2, before.s2)
+    assert np.array_equal(t.heaps[0].tsdf[lo:lo + n], vals)
+    heap.weight[lo + 5] = 7.0
+    assert t.payload(coord).weight[5] == 7.0 and np.array_equal(t.payload(coord).tsdf, vals)
+    heap.color[lo:lo + n] = 0.5
+    assert np.all(t.payload(coord).color == 0.5)
+    dead = int(np.nonzero(~t.heaps[0].live)[0][0])
+    with pytest.raises(ValueError):
+        t.heaps[0].tsdf[dead * n] = 1.0
+    with pytest.raises(ValueError):
+        t.heaps[0].tsdf[lo:lo + n][0] = 1.0
+    cp = t.heaps[0].tsdf.copy()
+    cp[0] = 3.0  # a copy is an ordinary array
 
 
 def test_c5_two_million_point_scan_vs_oracle():
@@ -774,7 +810,7 @@ def test_walk_cluster_dsmem_filter_matches_oracle():
         "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
         "import numpy as np, parity_utils as PU\n"
         "spec = dict(scene='large_room', frames=3, width=160, height=120, edge=0.04, tau=0.015,\n"
-        "            caps=(60000, 10000, 4000), n_hash=1000003, sigma=2.5e-5, cadence=3, all_levels=True,\n"
+        "            caps=(400000, 10000, 4000), n_hash=1000003, sigma=2.5e-5, cadence=3, all_levels=True,\n"
         "            depth_dtype=np.float32, color_dtype=np.uint8)\n"
         "g, sg, mg, _ = PU.run_depth_scenario('gpu', **spec)\n"
         "o, so, mo, _ = PU.run_depth_scenario('oracle', **spec)\n"
