@@ -80,6 +80,9 @@ struct Table {
   Buf batch, pyr, lidar_aux;
   Buf dblk, dmicro, dexact;  // depth update work lists (blocks, micro-bricks, voxels)
   Buf mdev;                  // MergeDev of the last enqueued merge pass
+  // canonical allocation order: ranks by key (kept all-zero between uses),
+  // for new blocks and for merge candidates, and the sorted candidates
+  Buf rank_buf, rank_m, cand_sorted;
   Buf lidar_hot;             // LiDAR hot-segment chunk offsets + hit masks
   // depth batches overlap frame k+1's allocation (walk stream) with frame
   // k's voxel update (main stream): per-parity copies of the frame scratch

@@ -99,9 +99,35 @@ def summarize(xml: Path) -> dict:
     return {"counts": counts, "cases": cases}
 
 
+def report(summary_json: Path, out_md: Path) -> None:
+    """Markdown summary of a run (per file counts, every non-pass)."""
+    import collections
+    d = json.loads(Path(summary_json).read_text())
+    per = collections.defaultdict(collections.Counter)
+    for c in d["cases"]:
+        per[c["file"].split(".")[0] or "(collection)"][c["status"]] += 1
+    lines = ["# The reference's own test suite against this package (B200)", "",
+             "`scripts/reference_suite.py run` on a gpurun box: the reference's unmodified "
+             "`tests/` with `tsdfusion` mapped to `paper_2511_21459_b200` "
+             f"({d.get('wall_s', '?')} s).", "",
+             f"**{d['counts']['passed']} passed, {d['counts']['failed']} failed, "
+             f"{d['counts']['error']} errors, {d['counts']['skipped']} skipped.**", "",
+             "| file | passed | failed | error | skipped |", "|---|---|---|---|---|"]
+    for f in sorted(per):
+        c = per[f]
+        lines.append(f"| {f} | {c['passed']} | {c['failed']} | {c['error']} | {c['skipped']} |")
+    bad = [c for c in d["cases"] if c["status"] in ("failed", "error", "skipped")]
+    if bad:
+        lines += ["", "Not passing:", ""]
+        lines += [f"- `{c['file']}::{c['name']}` ({c['status']}): {c['message']}" for c in bad]
+    Path(out_md).write_text("\n".join(lines) + "\n")
+
+
 if __name__ == "__main__":
     mode = sys.argv[1] if len(sys.argv) > 1 else "run"
     if mode == "stage":
         stage()
+    elif mode == "report":
+        report(Path(sys.argv[2]), Path(sys.argv[3]))
     else:
         sys.exit(run())

@@ -722,6 +722,41 @@ def test_heap_snapshots_are_cached_per_map_version():
     assert t.heaps[0].occupied == int(t.heaps[0].live.sum())
 
 
+def _handles(backend):
+    if backend.name == "oracle":
+        return {l: backend.t.live_blocks(l) for l in range(backend.t.num_levels)}
+    out = {}
+    for l in range(backend.t.num_levels):
+        coords, handles = backend.t.export_level(l)[:2]
+        out[l] = (coords, handles)
+    return out
+
+
+@pytest.mark.parametrize("kind", ["depth", "lidar"])
+def test_heap_handles_follow_the_references_allocation_order(kind):
+    """New blocks take heap handles in ascending (x, y, z) order (the
+    reference's np.unique + _ensure_blocks, integrate.py:203 / :289) and a
+    merge pass re-homes candidates in the same order (adapt.py:130-135), so
+    the heap layout -- not just the canonical state -- equals the oracle's,
+    and two runs give the same layout (the reference's deterministic rerun,
+    tests/test_integrate.py:273-288)."""
+    if kind == "depth":
+        spec = dict(scene="sphere", frames=20, width=64, height=48, edge=0.08, tau=0.03,
+                    caps=(30000, 10000), n_hash=100003, sigma=2.5e-4, cadence=10)
+        runs = [PU.run_depth_scenario(b, **spec) for b in ("gpu", "gpu", "oracle")]
+    else:
+        spec = dict(scans=3, beams=32, columns=256, edge=1.6, tau=0.8, caps=(200000, 20000),
+                    n_hash=1000003, sigma=1e-2, cadence=2)
+        runs = [PU.run_lidar_scenario(b, **spec) for b in ("gpu", "gpu", "oracle")]
+    assert runs[0][1] == runs[2][1] and runs[0][2] == runs[2][2]
+    assert sum(m["merged"] for m in runs[2][2]) > 0
+    h = [_handles(r[0]) for r in runs]
+    for l in h[2]:
+        for a, b in ((h[0], h[2]), (h[1], h[2])):
+            assert np.array_equal(a[l][0], b[l][0]), f"level {l} coords"
+            assert np.array_equal(a[l][1], b[l][1]), f"level {l} handles"
+
+
 def test_heap_voxel_arrays_write_through_like_the_reference():
     """heaps[l].tsdf[a:b] = x (how the reference's own tests craft fields,
     tests/test_meshing.py:22-39) writes the touched live blocks to the
