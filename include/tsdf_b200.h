@@ -314,7 +314,8 @@ int tsdf_import_level(tsdf_table *t, int32_t level, const int64_t *coords, int64
                       const double *tsdf, const double *weight, const double *s2,
                       const float *color);
 
-/* BlockHeap.occupied for one level */
+/* BlockHeap.occupied for one level; level -1: HashTable.live_count (every
+ * level, one read-back) */
 int tsdf_live_count(tsdf_table *t, int32_t level, int64_t *n);
 /* all live blocks of a level in canonical (x, y, z) order with their
  * payloads (parity export / save_map).  Call with coords == NULL to get the

@@ -83,6 +83,11 @@ struct Table {
   // canonical allocation order: ranks by key (kept all-zero between uses),
   // for new blocks and for merge candidates, and the sorted candidates
   Buf rank_buf, rank_m, cand_sorted;
+  // single-block calls (find / insert / remove / payload): one device staging
+  // area and its pinned host twin, so a call is one or two round trips
+  Buf blk_dev;
+  void* blk_host = nullptr;
+  size_t blk_host_bytes = 0;
   Buf lidar_hot;             // LiDAR hot-segment chunk offsets + hit masks
   // depth batches overlap frame k+1's allocation (walk stream) with frame
   // k's voxel update (main stream): per-parity copies of the frame scratch

@@ -255,7 +255,9 @@ class HashTable:
         return self.block_edge / voxel_side(level)
 
     def live_count(self) -> int:
-        return sum(h.occupied for h in self.heaps)
+        n = C.c_int64()
+        N.check(N.lib().tsdf_live_count(self._h, -1, C.byref(n)), "live_count")
+        return int(n.value)
 
     def fill_fractions(self) -> list:
         return [h.fill_fraction() for h in self.heaps]
@@ -376,18 +378,21 @@ class HashTable:
         return int(out.value)
 
     def _payload_call(self, fn, coord, what):
-        c = np.asarray(coord, dtype=np.int64).reshape(3)
-        found = self.find(c)
-        if found is None:
-            raise NotFoundError(f"block {tuple(int(v) for v in c)} is not live")
-        nvox = self.heaps[found[1]].nvox
-        t, w, s2 = np.zeros(nvox), np.zeros(nvox), np.zeros(nvox)
-        col = np.zeros((nvox, 3), dtype=np.float32)
+        # one library call: buffers sized for the finest level, trimmed to
+        # the level the call reports (two device round trips, no find first)
+        c = np.ascontiguousarray(np.asarray(coord, dtype=np.int64).reshape(3))
+        nmax = self.heaps[0].nvox
+        t, w, s2 = np.zeros(nmax), np.zeros(nmax), np.zeros(nmax)
+        col = np.zeros((nmax, 3), dtype=np.float32)
         lv = C.c_int32()
-        N.check(fn(self._h, c, C.byref(lv), t.ctypes.data, w.ctypes.data, s2.ctypes.data,
-                   col.ctypes.data), what)
-        return BlockPayload(coord=tuple(int(v) for v in c), level=int(lv.value), tsdf=t,
-                            weight=w, s2=s2, color=col)
+        try:
+            N.check(fn(self._h, c, C.byref(lv), t.ctypes.data, w.ctypes.data, s2.ctypes.data,
+                       col.ctypes.data), what)
+        except NotFoundError:
+            raise NotFoundError(f"block {tuple(int(v) for v in c)} is not live") from None
+        n = self.heaps[int(lv.value)].nvox
+        return BlockPayload(coord=tuple(int(v) for v in c), level=int(lv.value), tsdf=t[:n].copy(),
+                            weight=w[:n].copy(), s2=s2[:n].copy(), color=col[:n].copy())
 
     def remove(self, coord) -> BlockPayload:
         return self._payload_call(N.lib().tsdf_remove, coord, "remove")

@@ -13,9 +13,9 @@ tests/ (which compares against the oracle and reference-generated goldens).
 The staged copy lives under oracle/_ref/ (git-ignored, like the compiled
 reference: it travels to the GPU box with the snapshot but never enters the
 repository history).  Modules the tier leaves out of scope (the CLI and the
-reference's own benchmark/report driver) are not aliased, so the
-two test files importing them report as collection errors; everything else
-runs.
+reference's own benchmark/report driver) are stubs that raise
+NotImplementedError when called, so only the tests that call them fail and
+the rest of their files run.
 """
 from __future__ import annotations
 
@@ -51,6 +51,20 @@ def stage() -> None:
     print(f"staged {len(list(STAGE.glob('test_*.py')))} test files into {STAGE}")
 
 
+def _out_of_scope_stub(name: str, attrs) -> None:
+    """A placeholder for a reference module this tier does not rebuild (the
+    CLI, the benchmark driver): importing it works, so the other tests of
+    the same file run; calling into it fails loudly."""
+    import types
+    mod = types.ModuleType(f"tsdfusion.{name}")
+
+    def _missing(*_a, **_k):
+        raise NotImplementedError(f"tsdfusion.{name} is out of scope for this tier (SURVEY §2)")
+    for a in attrs:
+        setattr(mod, a, _missing)
+    sys.modules[f"tsdfusion.{name}"] = mod
+
+
 def alias() -> None:
     sys.path.insert(0, str(ROOT))
     pkg = importlib.import_module("paper_2511_21459_b200")
@@ -59,6 +73,8 @@ def alias() -> None:
         mod = importlib.import_module(f"paper_2511_21459_b200.{ours}")
         sys.modules[f"tsdfusion.{ref_name}"] = mod
         setattr(pkg, ref_name, mod)
+    _out_of_scope_stub("cli", ["main"])
+    _out_of_scope_stub("bench", ["bench_config", "run_bench"])
 
 
 def run() -> int:
@@ -116,6 +132,10 @@ def report(summary_json: Path, out_md: Path) -> None:
     for f in sorted(per):
         c = per[f]
         lines.append(f"| {f} | {c['passed']} | {c['failed']} | {c['error']} | {c['skipped']} |")
+    lines += ["", "`tsdfusion.cli` and `tsdfusion.bench` (the CLI and the reference's benchmark "
+              "driver) are out of scope for this tier (SURVEY §2): they are stubs that raise "
+              "NotImplementedError, so the tests calling them fail and the rest of "
+              "`test_pipeline.py` / `test_acceptance.py` run."]
     bad = [c for c in d["cases"] if c["status"] in ("failed", "error", "skipped")]
     if bad:
         lines += ["", "Not passing:", ""]

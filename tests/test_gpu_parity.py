@@ -791,6 +791,45 @@ def test_heap_voxel_arrays_write_through_like_the_reference():
     cp[0] = 3.0  # a copy is an ordinary array
 
 
+def test_heap_payload_by_handle_and_probe_length():
+    """BlockHeap.payload / write_payload by handle (hashgrid.py:115-133) and
+    HashTable.probe_length (hashgrid.py:194-212): a handle addresses the
+    same block as its coordinate; a free handle reads as zeros and cannot be
+    written; n_hash >= 4x live blocks keeps mean probes <= 2 (the
+    reference's own bound, tests/test_hashgrid.py:220-230)."""
+    import paper_2511_21459_b200 as P
+    from paper_2511_21459_b200.hashgrid import BlockPayload
+    rng = np.random.default_rng(100)
+    t = P.HashTable(4099, 10, 7, 0.08, (600, 8))
+    seen, coords = set(), []
+    while len(coords) < 600:
+        c = tuple(int(v) for v in rng.integers(-1000, 1000, size=3))
+        if c not in seen:
+            seen.add(c)
+            coords.append(c)
+    for c in coords:
+        t.insert(c, 0)
+    probes = t.probe_lengths(coords)
+    assert probes.min() >= 1 and probes.mean() <= 2.0
+    assert t.probe_length(coords[7]) == probes[7]
+    heap = t.heaps[0]
+    h, lv = t.find(coords[5])
+    assert lv == 0
+    p = heap.payload(h)
+    assert p.coord == coords[5] and p.level == 0 and not p.tsdf.any()
+    new = BlockPayload(coord=coords[5], level=0, tsdf=np.full(heap.nvox, 0.01),
+                       weight=np.full(heap.nvox, 2.0), s2=np.zeros(heap.nvox),
+                       color=np.full((heap.nvox, 3), 0.25, dtype=np.float32))
+    heap.write_payload(h, new)
+    back = t.payload(coords[5])
+    assert np.array_equal(back.tsdf, new.tsdf) and np.array_equal(back.weight, new.weight)
+    t.remove(coords[9])
+    free_h = int(np.nonzero(~t.heaps[0].live)[0][0])
+    assert not t.heaps[0].payload(free_h).tsdf.any()
+    with pytest.raises(ValueError):
+        t.heaps[0].write_payload(free_h, new)
+
+
 def test_c5_two_million_point_scan_vs_oracle():
     """BASELINE config 5's LiDAR part: one 128 x 16384-column scan (~2 M
     returns, 100 m range, 1.6 m blocks) against the oracle -- stats and the
