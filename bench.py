@@ -108,6 +108,7 @@ class ClockSampler:
         self.index = index
         self.rows = []  # (sm_mhz, max_mhz, [4 reason flags])
         self._stop = threading.Event()
+        self._ready = threading.Event()  # set once the first sample is in
 
     def _run_nvml(self, nv):
         h = nv.nvmlDeviceGetHandleByIndex(self.index)
@@ -118,6 +119,7 @@ class ClockSampler:
             sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.rows.append((float(sm), float(mx), [bool(r & b) for b in bits]))
+            self._ready.set()
             self._stop.wait(0.002)
 
     def _run_smi(self):
@@ -129,6 +131,7 @@ class ClockSampler:
                 r = [x.strip() for x in out.split(",")]
                 if len(r) >= 6 and r[0].replace(".", "").isdigit():
                     self.rows.append((float(r[0]), float(r[1]), [x == "Active" for x in r[2:6]]))
+                    self._ready.set()
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -147,8 +150,11 @@ class ClockSampler:
             self._run_smi()
 
     def __enter__(self):
+        # NVML initialisation can take longer than a short timed region: the
+        # region starts only after the sampler has its first reading
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
+        self._ready.wait(timeout=10.0)
         return self
 
     def __exit__(self, *a):
