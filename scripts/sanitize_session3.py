@@ -19,14 +19,15 @@ from paper_2511_21459_b200 import synth  # noqa: E402
 
 def main():
     # depth: single calls, then a window, then merges (3 levels)
-    frames = synth.render_frames("sphere", 12, 48, 36, depth_dtype=np.float32, color_dtype=np.uint8)
-    t = P.HashTable(100003, 10, 7, 0.08, (20000, 8000, 4000))
-    for f in frames[:6]:
+    frames = synth.render_frames("sphere", 20, 64, 48, depth_dtype=np.float32, color_dtype=np.uint8)
+    t = P.HashTable(100003, 10, 7, 0.08, (30000, 10000, 4000))
+    for f in frames[:10]:
         P.integrate_depth(t, f, 0.03)
+    ms0 = P.apply_merges(t, 2.5e-4, all_levels=True)
     from paper_2511_21459_b200.integrate import integrate_depth_window
-    _, ms0 = integrate_depth_window(t, frames[6:], 0.03, 2.5e-4, all_levels=True)
-    ms = P.apply_merges(t, 2.5e-4, all_levels=True)
+    _, ms = integrate_depth_window(t, frames[10:], 0.03, 2.5e-4, all_levels=True)
     print("depth", t.live_count(), ms0.merged, ms.merged)
+    assert ms0.merged > 0 and ms.merged > 0
     # LiDAR (walk with near pairs; 64-bit keys)
     scan = synth.lidar_frames(1, 16, 256)[0]
     tl = P.HashTable(1000003, 10, 7, 1.6, (100000, 10000))
